@@ -1,0 +1,131 @@
+/*
+ * simplicial_attn.h -- C ABI of the B200 (sm_100a) sliding-window 2-simplicial attention library
+ * (libsimplicial.so).  arXiv 2507.02754; citations "P:n" are PAPER.md lines with their section.
+ *
+ * OPERATION (forward, Sec. 4; windows P:319-321 Sec. 6, masks P:804-812 App. B):
+ *   for every batch b, head h, query row i (key position pos = n_prefix + i):
+ *     W1(i) = { j : max(0, pos-w1+1) <= j <= pos },  W2(i) = { k : max(0, pos-w2+1) <= k <= pos }
+ *     A_ijk = s * sum_l q_il k_jl k2_kl                           (trilinear, Eq. 3d-attention)
+ *     A_ijk = s * sum_{l<p} det[q_i^(l); k_j^(l); k2_k^(l)]        (SA_VARIANT_DET, Eq. logits)
+ *             p = floor(D/3); the trailing D mod 3 dims do not enter the logits
+ *     lse_i = log sum_{j in W1, k in W2} exp(A_ijk)                (natural log, fp32)
+ *     o_i   = sum_{j,k} exp(A_ijk - lse_i) (v_j o v2_k)            (Eq. softmax/attenval P:236-244)
+ *   s = 1/sqrt(D); there is no scale argument and no K2/V2 bias.
+ * BACKWARD (Sec. 7, corrected as in DESIGN.md): with delta_i = <dO_i, o_i>,
+ *   dP_ijk = sum_d dO_id v_jd v2_kd,  dS_ijk = P_ijk (dP_ijk - delta_i),
+ *   dq_i = s sum_jk dS k_j o k2_k,  dk_j = s sum_ik dS q_i o k2_k,  dk2_k = s sum_ij dS q_i o k_j,
+ *   dv_j = sum_ik P dO_i o v2_k,   dv2_k = sum_ij P dO_i o v_j
+ *   (SA_VARIANT_DET: the products a o b in dq/dk/dk2 become chunkwise cross products
+ *    k_j x k2_k, k2_k x q_i, q_i x k_j, zero on the trailing D mod 3 dims).
+ *
+ * LAYOUT.  All tensor pointers are DEVICE pointers, allocated and owned by the caller.
+ *   q, o, dO, dq          : [B, N, H, D] contiguous, D fastest   (query side)
+ *   k, v, k2, v2, dk..dv2 : [B, n_prefix+N, H, D] contiguous     (key side)
+ *   lse                   : [B, H, N] fp32
+ *   Input dtype (q,k,v,k2,v2,dO): bf16, or fp32 with SA_IN_F32.
+ *   Output dtype (o, dq, dk, dv, dk2, dv2): fp32 if SA_OUT_F32 or SA_IN_F32, else bf16.
+ *   The backward reads o in the output dtype.
+ * OWNERSHIP.  The library never allocates device memory; the backward workspace is caller-provided
+ *   (size from simplicial_attn_bwd_workspace_bytes).  Outputs must not alias inputs.
+ * EXECUTION.  Asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy default
+ *   stream).  Results are valid after the caller synchronises.  Deterministic: no atomics on the
+ *   data path, identical bits run to run.  Stateless and thread-safe (only cached driver entry
+ *   points and a launch counter are global).
+ * ERRORS.  Returned synchronously before any launch: null pointers, B,H,N,D < 1, w1,w2 < 1,
+ *   n_prefix < 0, DET with D < 3 -> SA_ERR_INVALID_ARG; D > 128 -> SA_ERR_UNSUPPORTED; workspace
+ *   too small -> SA_ERR_WORKSPACE.  A window w > n_prefix+N is accepted and clamps.  Launch failures
+ *   (cudaGetLastError) -> SA_ERR_CUDA.  Asynchronous faults surface at the caller's sync.  No C++
+ *   exception crosses the ABI.
+ */
+#ifndef SIMPLICIAL_ATTN_H
+#define SIMPLICIAL_ATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SA_OK = 0,
+  SA_ERR_INVALID_ARG = 1,
+  SA_ERR_UNSUPPORTED = 2,
+  SA_ERR_WORKSPACE = 3,
+  SA_ERR_CUDA = 4
+} sa_status;
+
+enum {
+  SA_VARIANT_DET = 1u << 0, /* 0: trilinear (Eq. 3d-attention); 1: sum of 3x3 dets (Eq. logits) */
+  SA_IN_F32 = 1u << 1,      /* inputs fp32 (exact fp32 SIMT path); default bf16 inputs               */
+  SA_OUT_F32 = 1u << 2,     /* outputs/gradients fp32 (parity runs); default = input dtype           */
+  SA_FORCE_SIMT = 1u << 3   /* diagnostics: force the fp32 CUDA-core kernels even for bf16 inputs    */
+};
+
+/* Kernel families the dispatcher can select (simplicial_attn_fwd_path / _bwd_path). */
+enum { SA_PATH_SIMT = 1, SA_PATH_TCGEN05 = 2 };
+
+/* Forward.  Writes o [B,N,H,D] and lse [B,H,N]. */
+sa_status simplicial_attn_fwd(const void* q, const void* k, const void* v, const void* k2,
+                              const void* v2, void* o, float* lse, int64_t B, int64_t H, int64_t N,
+                              int64_t D, int64_t w1, int64_t w2, uint32_t flags, void* stream);
+
+/* Sequence-sharded forward: k, v, k2, v2 carry n_prefix leading key-only rows
+ * ([B, n_prefix+N, H, D]); query row i sits at key position n_prefix+i.  n_prefix = 0 is
+ * simplicial_attn_fwd. */
+sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void* v, const void* k2,
+                                       const void* v2, void* o, float* lse, int64_t B, int64_t H,
+                                       int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                       int64_t n_prefix, uint32_t flags, void* stream);
+
+/* Bytes of device workspace the backward needs (delta_i [B,H,N] fp32 plus kernel scratch). */
+size_t simplicial_attn_bwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                           int64_t w2, uint32_t flags);
+
+/* Backward.  Reads o (output dtype) and lse from the forward; writes dq [B,N,H,D] and
+ * dk, dv, dk2, dv2 over all n_prefix+N key rows (rows no query touches are written as 0). */
+sa_status simplicial_attn_bwd(const void* q, const void* k, const void* v, const void* k2,
+                              const void* v2, const void* o, const float* lse, const void* dO,
+                              void* dq, void* dk, void* dv, void* dk2, void* dv2, void* workspace,
+                              size_t workspace_bytes, int64_t B, int64_t H, int64_t N, int64_t D,
+                              int64_t w1, int64_t w2, uint32_t flags, void* stream);
+
+sa_status simplicial_attn_bwd_prefixed(const void* q, const void* k, const void* v, const void* k2,
+                                       const void* v2, const void* o, const float* lse,
+                                       const void* dO, void* dq, void* dk, void* dv, void* dk2,
+                                       void* dv2, void* workspace, size_t workspace_bytes,
+                                       int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                       int64_t w2, int64_t n_prefix, uint32_t flags, void* stream);
+
+/* End-to-end step from HOST buffers: copies the six inputs host->device into the caller's device
+ * scratch, runs forward and backward, and copies o, lse and the five gradients device->host, all
+ * on `stream` (pinned host memory makes the copies asynchronous).  Host layouts/dtypes as above
+ * (n_prefix = 0).  d_scratch must hold simplicial_attn_host_step_scratch_bytes(...) bytes. */
+size_t simplicial_attn_host_step_scratch_bytes(int64_t B, int64_t H, int64_t N, int64_t D,
+                                               int64_t w1, int64_t w2, uint32_t flags);
+sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void* h_v,
+                                    const void* h_k2, const void* h_v2, const void* h_dO,
+                                    void* h_o, float* h_lse, void* h_dq, void* h_dk, void* h_dv,
+                                    void* h_dk2, void* h_dv2, void* d_scratch, size_t scratch_bytes,
+                                    int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                    int64_t w2, uint32_t flags, void* stream);
+
+/* Which kernel family the dispatcher picks for these arguments (SA_PATH_*), 0 if unsupported. */
+int simplicial_attn_fwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                             uint32_t flags);
+int simplicial_attn_bwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                             uint32_t flags);
+
+/* Total kernels this library has launched since it was loaded (for the bench's gpu_launches). */
+uint64_t simplicial_attn_launch_count(void);
+
+const char* simplicial_attn_status_string(sa_status s);
+
+/* Library build identifier (compile target and date), e.g. "sm_100a ...". */
+const char* simplicial_attn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIMPLICIAL_ATTN_H */

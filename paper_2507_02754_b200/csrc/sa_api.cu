@@ -1,0 +1,233 @@
+// sa_api.cu -- the C ABI (include/simplicial_attn.h): validation, kernel selection, launches.
+#include <atomic>
+#include <math.h>
+#include <stdio.h>
+
+#include "sa_common.cuh"
+
+namespace sa {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(uint64_t(n), std::memory_order_relaxed); }
+
+cudaError_t simt_forward(const Problem& p, bool in_f32, bool out_f32, const void* q, const void* k,
+                         const void* v, const void* k2, const void* v2, void* o, float* lse, cudaStream_t st);
+cudaError_t simt_backward(const Problem& p, bool in_f32, bool out_f32, const void* q, const void* k,
+                          const void* v, const void* k2, const void* v2, const void* o, const float* lse,
+                          const void* dO, void* dq, void* dk, void* dv, void* dk2, void* dv2, float* delta,
+                          cudaStream_t st);
+
+// tcgen05 path (sa_tc_fwd.cu / sa_tc_bwd.cu)
+bool tc_fwd_supported(const Problem& p);
+cudaError_t tc_forward(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
+                       const void* k2, const void* v2, void* o, float* lse, cudaStream_t st);
+bool tc_bwd_supported(const Problem& p);
+size_t tc_bwd_workspace_bytes(const Problem& p);
+cudaError_t tc_backward(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
+                        const void* k2, const void* v2, const void* o, const float* lse, const void* dO,
+                        void* dq, void* dk, void* dv, void* dk2, void* dv2, void* ws, size_t ws_bytes,
+                        cudaStream_t st);
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Validate scalar arguments; fill the Problem.  Rejects before any launch.
+static sa_status make_problem(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                              int64_t n_prefix, uint32_t flags, Problem* p) {
+  if (B < 1 || H < 1 || N < 1 || D < 1 || w1 < 1 || w2 < 1 || n_prefix < 0) return SA_ERR_INVALID_ARG;
+  if ((flags & SA_VARIANT_DET) && D < 3) return SA_ERR_INVALID_ARG;
+  if (flags & ~uint32_t(SA_VARIANT_DET | SA_IN_F32 | SA_OUT_F32 | SA_FORCE_SIMT)) return SA_ERR_INVALID_ARG;
+  if (D > 128) return SA_ERR_UNSUPPORTED;
+  int64_t NK = n_prefix + N;
+  if (NK > (int64_t(1) << 30) || B * H > 65535 || NK > 2147483647 / 4) return SA_ERR_UNSUPPORTED;
+  // windows longer than the key buffer clamp
+  if (w1 > NK) w1 = NK;
+  if (w2 > NK) w2 = NK;
+  p->B = int(B); p->H = int(H); p->N = int(N); p->D = int(D);
+  p->w1 = int(w1); p->w2 = int(w2); p->np = int(n_prefix);
+  p->det = (flags & SA_VARIANT_DET) != 0;
+  p->scale = float(1.0 / sqrt(double(D)));
+  return SA_OK;
+}
+
+static bool use_tc_fwd(const Problem& p, uint32_t flags) {
+  if (flags & (SA_IN_F32 | SA_FORCE_SIMT)) return false;
+  return tc_fwd_supported(p);
+}
+static bool use_tc_bwd(const Problem& p, uint32_t flags) {
+  if (flags & (SA_IN_F32 | SA_FORCE_SIMT)) return false;
+  return tc_bwd_supported(p);
+}
+
+static size_t bwd_ws(const Problem& p, uint32_t flags) {
+  size_t base = align256(sizeof(float) * size_t(p.B) * p.H * p.N);  // delta
+  if (use_tc_bwd(p, flags)) base += align256(tc_bwd_workspace_bytes(p));
+  return base;
+}
+
+static sa_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return SA_OK;
+  fprintf(stderr, "[simplicial_attn] CUDA error: %s\n", cudaGetErrorString(e));
+  return SA_ERR_CUDA;
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" {
+
+sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void* v, const void* k2,
+                                       const void* v2, void* o, float* lse, int64_t B, int64_t H,
+                                       int64_t N, int64_t D, int64_t w1, int64_t w2, int64_t n_prefix,
+                                       uint32_t flags, void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse) return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p);
+  if (s != SA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  cudaGetLastError();  // clear stale errors so a failure below is ours
+  if (use_tc_fwd(p, flags)) return cuda_status(tc_forward(p, out_f32, q, k, v, k2, v2, o, lse, st));
+  return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
+}
+
+sa_status simplicial_attn_fwd(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                              void* o, float* lse, int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                              int64_t w2, uint32_t flags, void* stream) {
+  return simplicial_attn_fwd_prefixed(q, k, v, k2, v2, o, lse, B, H, N, D, w1, w2, 0, flags, stream);
+}
+
+size_t simplicial_attn_bwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                           uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
+  return bwd_ws(p, flags);
+}
+
+sa_status simplicial_attn_bwd_prefixed(const void* q, const void* k, const void* v, const void* k2,
+                                       const void* v2, const void* o, const float* lse, const void* dO,
+                                       void* dq, void* dk, void* dv, void* dk2, void* dv2, void* workspace,
+                                       size_t workspace_bytes, int64_t B, int64_t H, int64_t N, int64_t D,
+                                       int64_t w1, int64_t w2, int64_t n_prefix, uint32_t flags,
+                                       void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse || !dO || !dq || !dk || !dv || !dk2 || !dv2 || !workspace)
+    return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p);
+  if (s != SA_OK) return s;
+  if (workspace_bytes < bwd_ws(p, flags)) return SA_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  float* delta = (float*)workspace;
+  cudaGetLastError();
+  if (use_tc_bwd(p, flags))  // workspace: delta first, then the tcgen05 kernels' scratch
+    return cuda_status(tc_backward(p, out_f32, q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2,
+                                   workspace, workspace_bytes, st));
+  return cuda_status(simt_backward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2,
+                                   delta, st));
+}
+
+sa_status simplicial_attn_bwd(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                              const void* o, const float* lse, const void* dO, void* dq, void* dk, void* dv,
+                              void* dk2, void* dv2, void* workspace, size_t workspace_bytes, int64_t B,
+                              int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2, uint32_t flags,
+                              void* stream) {
+  return simplicial_attn_bwd_prefixed(q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2, workspace,
+                                      workspace_bytes, B, H, N, D, w1, w2, 0, flags, stream);
+}
+
+// Device scratch layout of the host step: 6 inputs | o | lse | 5 grads | bwd workspace.
+static size_t host_step_layout(const Problem& p, uint32_t flags, size_t off[16]) {
+  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  size_t ein = in_f32 ? 4 : 2, eout = out_f32 ? 4 : 2;
+  size_t nel = size_t(p.B) * p.N * p.H * p.D;
+  size_t cur = 0;
+  for (int t = 0; t < 6; ++t) { off[t] = cur; cur += align256(nel * ein); }
+  off[6] = cur; cur += align256(nel * eout);                               // o
+  off[7] = cur; cur += align256(sizeof(float) * size_t(p.B) * p.H * p.N);  // lse
+  for (int t = 8; t < 13; ++t) { off[t] = cur; cur += align256(nel * eout); }
+  off[13] = cur; cur += align256(bwd_ws(p, flags));
+  off[14] = cur;
+  return cur;
+}
+
+size_t simplicial_attn_host_step_scratch_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                               int64_t w2, uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
+  size_t off[16];
+  return host_step_layout(p, flags, off);
+}
+
+sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void* h_v, const void* h_k2,
+                                    const void* h_v2, const void* h_dO, void* h_o, float* h_lse, void* h_dq,
+                                    void* h_dk, void* h_dv, void* h_dk2, void* h_dv2, void* d_scratch,
+                                    size_t scratch_bytes, int64_t B, int64_t H, int64_t N, int64_t D,
+                                    int64_t w1, int64_t w2, uint32_t flags, void* stream) {
+  const void* hin[6] = {h_q, h_k, h_v, h_k2, h_v2, h_dO};
+  void* hout[5] = {h_dq, h_dk, h_dv, h_dk2, h_dv2};
+  for (auto x : hin) if (!x) return SA_ERR_INVALID_ARG;
+  for (auto x : hout) if (!x) return SA_ERR_INVALID_ARG;
+  if (!h_o || !h_lse || !d_scratch) return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem(B, H, N, D, w1, w2, 0, flags, &p);
+  if (s != SA_OK) return s;
+  size_t off[16];
+  size_t need = host_step_layout(p, flags, off);
+  if (scratch_bytes < need) return SA_ERR_WORKSPACE;
+  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  size_t nel = size_t(p.B) * p.N * p.H * p.D;
+  size_t bin = nel * (in_f32 ? 4 : 2), bout = nel * (out_f32 ? 4 : 2);
+  size_t blse = sizeof(float) * size_t(p.B) * p.H * p.N;
+  char* base = (char*)d_scratch;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaGetLastError();
+  for (int t = 0; t < 6; ++t) {
+    cudaError_t e = cudaMemcpyAsync(base + off[t], hin[t], bin, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  s = simplicial_attn_fwd(base + off[0], base + off[1], base + off[2], base + off[3], base + off[4],
+                          base + off[6], (float*)(base + off[7]), B, H, N, D, w1, w2, flags, stream);
+  if (s != SA_OK) return s;
+  s = simplicial_attn_bwd(base + off[0], base + off[1], base + off[2], base + off[3], base + off[4],
+                          base + off[6], (const float*)(base + off[7]), base + off[5], base + off[8],
+                          base + off[9], base + off[10], base + off[11], base + off[12], base + off[13],
+                          off[14] - off[13], B, H, N, D, w1, w2, flags, stream);
+  if (s != SA_OK) return s;
+  cudaError_t e = cudaMemcpyAsync(h_o, base + off[6], bout, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_lse, base + off[7], blse, cudaMemcpyDeviceToHost, st);
+  for (int t = 0; t < 5 && e == cudaSuccess; ++t)
+    e = cudaMemcpyAsync(hout[t], base + off[8 + t], bout, cudaMemcpyDeviceToHost, st);
+  return cuda_status(e);
+}
+
+int simplicial_attn_fwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                             uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
+  return use_tc_fwd(p, flags) ? SA_PATH_TCGEN05 : SA_PATH_SIMT;
+}
+
+int simplicial_attn_bwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                             uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
+  return use_tc_bwd(p, flags) ? SA_PATH_TCGEN05 : SA_PATH_SIMT;
+}
+
+uint64_t simplicial_attn_launch_count(void) { return g_launches.load(); }
+
+const char* simplicial_attn_status_string(sa_status s) {
+  switch (s) {
+    case SA_OK: return "SA_OK";
+    case SA_ERR_INVALID_ARG: return "SA_ERR_INVALID_ARG";
+    case SA_ERR_UNSUPPORTED: return "SA_ERR_UNSUPPORTED";
+    case SA_ERR_WORKSPACE: return "SA_ERR_WORKSPACE";
+    case SA_ERR_CUDA: return "SA_ERR_CUDA";
+  }
+  return "SA_UNKNOWN";
+}
+
+const char* simplicial_attn_version(void) { return "libsimplicial sm_100a " __DATE__ " " __TIME__; }
+
+}  // extern "C"

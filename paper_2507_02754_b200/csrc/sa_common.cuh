@@ -1,0 +1,49 @@
+// sa_common.cuh -- small device/host helpers shared by the library's kernels (not by the oracle).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/simplicial_attn.h"
+
+namespace sa {
+
+// Problem description handed to every kernel.  Key-side tensors have NK = np + N rows.
+struct Problem {
+  int B, H, N, D, w1, w2, np;  // np = n_prefix
+  float scale;                 // signed logit scale (negated when the DET operands are swapped)
+  bool det;
+  __host__ __device__ int NK() const { return np + N; }
+  // element offsets of row (b, pos, h) in query-side / key-side tensors
+  __host__ __device__ int64_t qoff(int b, int i, int h) const {
+    return ((int64_t(b) * N + i) * H + h) * D;
+  }
+  __host__ __device__ int64_t koff(int b, int j, int h) const {
+    return ((int64_t(b) * NK() + j) * H + h) * D;
+  }
+};
+
+__device__ __forceinline__ float ld_f(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ld_f(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void st_f(float* p, float x) { *p = x; }
+__device__ __forceinline__ void st_f(__nv_bfloat16* p, float x) { *p = __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// Window lower bound: key rows (pos - w, pos], clipped at 0.
+__host__ __device__ __forceinline__ int win_lo(int pos, int w) { return pos - w + 1 > 0 ? pos - w + 1 : 0; }
+
+// Launch bookkeeping (sa_api.cu).
+void note_launch(int n = 1);
+
+}  // namespace sa

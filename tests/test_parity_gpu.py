@@ -1,0 +1,153 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle, element by element,
+on the same seeded inputs.  Tolerances are the north star's: max abs 1e-4 for the fp32 path,
+2e-2 for the bf16-input path (outputs written in fp32, SA_OUT_F32; reading R20)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2507_02754_b200 import binding as sa
+from paper_2507_02754_b200.inputs import CONFIGS, make_inputs, seed_of
+from sa_testutil import TOL_BF16, TOL_F32, f64, maxabs, oracle_slice
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def run_cuda(inp, w1, w2, det, out_f32=True, n_prefix=0, force_simt=False, bwd=True):
+    t = {n: x.to(DEV) for n, x in inp.items()}
+    o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, det=det, out_f32=out_f32,
+                        n_prefix=n_prefix, force_simt=force_simt)
+    res = {"o": o, "lse": lse}
+    if bwd:
+        dq, dk, dv, dk2, dv2 = sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2,
+                                           det=det, out_f32=out_f32, n_prefix=n_prefix, force_simt=force_simt)
+        res.update(dq=dq, dk=dk, dv=dv, dk2=dk2, dv2=dv2)
+    torch.cuda.synchronize()
+    return res
+
+
+def run_oracle(inp, w1, w2, det, n_prefix=0, bwd=True):
+    a = {n: f64(x) for n, x in inp.items()}
+    o, lse = oracle.forward(a["q"], a["k"], a["v"], a["k2"], a["v2"], w1, w2, det=det, n_prefix=n_prefix)
+    res = {"o": o, "lse": lse}
+    if bwd:
+        g = oracle.backward(a["q"], a["k"], a["v"], a["k2"], a["v2"], a["dO"], w1, w2, det=det, n_prefix=n_prefix)
+        res.update(zip(("dq", "dk", "dv", "dk2", "dv2"), g))
+    return res
+
+
+def assert_close(got, ref, tol, names=("o", "lse", "dq", "dk", "dv", "dk2", "dv2")):
+    errs = {n: maxabs(got[n], ref[n]) for n in names if n in got}
+    bad = {n: e for n, e in errs.items() if not e <= tol}
+    assert not bad, f"max abs errors {errs} exceed {tol}"
+    return errs
+
+
+def test_c1_fp32_full():
+    """BASELINE config 1 (fp32, B=1 H=1 N=128 D=16 w1=32 w2=8), fwd+bwd, whole tensors."""
+    c = CONFIGS["c1"]
+    inp = make_inputs(c["B"], c["N"], c["H"], c["D"], seed_of("c1"), dtype="f32")
+    got = run_cuda(inp, c["w1"], c["w2"], False)
+    ref = run_oracle(inp, c["w1"], c["w2"], False)
+    assert_close(got, ref, TOL_F32)
+
+
+@pytest.mark.parametrize("det", [False, True])
+@pytest.mark.parametrize("B,N,H,D,w1,w2", [
+    (1, 1, 1, 16, 4, 4),        # single position
+    (2, 77, 3, 16, 9, 4),       # ragged N
+    (1, 64, 2, 32, 100, 3),     # window longer than the sequence (clamps)
+    (1, 96, 1, 48, 5, 17),      # w2 > w1
+    (1, 130, 2, 128, 33, 8),    # D = 128
+    (1, 50, 1, 7, 6, 6),        # D not a multiple of 3 or 32
+])
+def test_fp32_shapes(B, N, H, D, w1, w2, det):
+    inp = make_inputs(B, N, H, D, seed=N + D, dtype="f32")
+    got = run_cuda(inp, w1, w2, det)
+    ref = run_oracle(inp, w1, w2, det)
+    assert_close(got, ref, TOL_F32)
+
+
+@pytest.mark.parametrize("force_simt", [False, True])
+@pytest.mark.parametrize("det", [False, True])
+@pytest.mark.parametrize("B,N,H,D,w1,w2", [
+    (1, 384, 2, 128, 64, 32),
+    (1, 300, 1, 128, 128, 32),   # ragged tail, several tiles
+    (2, 256, 1, 64, 48, 16),     # D = 64
+    (1, 200, 1, 128, 40, 64),    # w2 = 64
+    (1, 160, 1, 128, 16, 48),    # w2 > w1
+])
+def test_bf16_shapes(B, N, H, D, w1, w2, det, force_simt):
+    inp = make_inputs(B, N, H, D, seed=7 * N + D, dtype="bf16")
+    got = run_cuda(inp, w1, w2, det, force_simt=force_simt)
+    ref = run_oracle(inp, w1, w2, det)
+    assert_close(got, ref, TOL_BF16)
+
+
+@pytest.mark.parametrize("det", [False, True])
+def test_bf16_outputs_in_bf16(det):
+    """Default output dtype (bf16) round-trips: compare against the oracle at the bf16 storage
+    tolerance (|x| up to ~10 rounds by up to 2^-5; reading R20)."""
+    inp = make_inputs(1, 256, 2, 128, seed=5, dtype="bf16")
+    got = run_cuda(inp, 64, 32, det, out_f32=False)
+    ref = run_oracle(inp, 64, 32, det)
+    for n in ("o", "dq", "dk", "dv", "dk2", "dv2"):
+        assert got[n].dtype == torch.bfloat16
+        err = np.abs(f64(got[n]) - ref[n]) - 2.0 ** -8 * np.abs(ref[n])
+        assert err.max() <= TOL_BF16, n
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", TOL_F32), ("bf16", TOL_BF16)])
+def test_prefixed_mode(dtype, tol):
+    """Sequence-sharded entry points: queries with a key halo as prefix."""
+    B, N, H, D, w1, w2, npf = 1, 160, 2, 64, 40, 16, 39
+    inp = make_inputs(B, N, H, D, seed=11, dtype=dtype, n_prefix=npf)
+    got = run_cuda(inp, w1, w2, False, n_prefix=npf)
+    ref = run_oracle(inp, w1, w2, False, n_prefix=npf)
+    assert_close(got, ref, tol)
+
+
+def test_deterministic():
+    inp = make_inputs(1, 300, 2, 128, seed=3, dtype="bf16")
+    a = run_cuda(inp, 128, 32, False)
+    b = run_cuda(inp, 128, 32, False)
+    for n in a:
+        assert torch.equal(a[n], b[n]), n
+
+
+def test_host_step_matches_device_path():
+    B, N, H, D, w1, w2 = 1, 256, 2, 128, 64, 32
+    inp = make_inputs(B, N, H, D, seed=17, dtype="bf16")
+    dev = run_cuda(inp, w1, w2, False)
+    h_in = {n: x.pin_memory() for n, x in inp.items()}
+    h_out = {n: torch.empty(dev[n].shape, dtype=dev[n].dtype).pin_memory() for n in dev}
+    sa.host_step(h_in, h_out, w1, w2, out_f32=True)
+    torch.cuda.synchronize()
+    for n in dev:
+        assert torch.equal(h_out[n], dev[n].cpu()), n
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_baseline_config_sampled(cfg):
+    """Full BASELINE sizes in the bench's launch configuration; the oracle checks sampled
+    (b, h, query-range) slices window-exactly (sa_testutil.oracle_slice)."""
+    c = CONFIGS[cfg]
+    inp = make_inputs(c["B"], c["N"], c["H"], c["D"], seed_of(cfg), dtype=c["dtype"],
+                      device="cpu")
+    got = run_cuda(inp, c["w1"], c["w2"], c["det"], bwd=c["bwd"])
+    N, L = c["N"], 96
+    rng = np.random.default_rng(0)
+    samples = [(0, 0, 0), (c["B"] - 1, c["H"] - 1, N - L)]
+    for _ in range(2):
+        samples.append((int(rng.integers(c["B"])), int(rng.integers(c["H"])), int(rng.integers(1, N - L))))
+    for b, h, a in samples:
+        ref = oracle_slice(inp, b, h, a, L, c["w1"], c["w2"], c["det"], c["bwd"])
+        assert maxabs(got["o"][b, a:a + L, h], ref["o"]) <= TOL_BF16
+        assert maxabs(got["lse"][b, h, a:a + L], ref["lse"]) <= TOL_BF16
+        if c["bwd"]:
+            assert maxabs(got["dq"][b, a:a + L, h], ref["dq"]) <= TOL_BF16
+            for n in ("dk", "dv", "dk2", "dv2"):
+                lo, hi, r = ref[n]
+                if hi > lo:
+                    assert maxabs(got[n][b, lo:hi, h], r) <= TOL_BF16, (n, b, h, a)
