@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark: sliding-window 2-simplicial attention fwd+bwd on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+A "step" is one forward + backward (every hot-path kernel) over one batch of synthetic
+inputs of BASELINE config c3 (B=4 H=16 N=8192 D=128 w1=512 w2=32, bf16 in) -- the
+configuration the metric's >=50%-of-peak target is quoted on.  N>1 runs under torchrun, one
+process per GPU: each rank processes its own c3-sized B*H shard (weak scaling, no data-path
+collective; NCCL only for the barrier and the max-over-ranks timing).
+
+FLOP bases:
+  paper formula (value): fwd 6*NW*D (Sec. 6), bwd 21*NW*D (7 backward einsums P:393-413
+      at the same 3-flop convention), NW = B*H*N*w1*w2 nominal triples;
+  tensor-core MMA (roofline): fwd 4*NW*D, bwd 14*NW*D (each einsum is one 2-flop contraction).
+``--impl reference`` times the float64 CPU oracle (oracle/) on a bounded sample of the same
+workload -- the reference arm of this tier (there is no runnable reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2507_02754_b200.inputs import CONFIGS, make_inputs, seed_of  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+PAPER_FLOPS_PER_TRIPLE_D = {"fwd": 6, "bwd": 21}
+MMA_FLOPS_PER_TRIPLE_D = {"fwd": 4, "bwd": 14}
+
+
+def peaks():
+    if os.path.exists(PEAKS_PATH):
+        p = json.load(open(PEAKS_PATH))
+        return p, "measured"
+    return FALLBACK_PEAKS, "fallback"
+
+
+def nominal_triples(c):
+    return c["B"] * c["H"] * c["N"] * c["w1"] * c["w2"]
+
+
+def paper_flops(c, which=("fwd", "bwd")):
+    return sum(PAPER_FLOPS_PER_TRIPLE_D[w] for w in which) * nominal_triples(c) * c["D"]
+
+
+# Algorithmic work of each library kernel per launch on config c:
+# (bound, unit, amount).  Tensor-core kernels: MMA flops of the contractions they own;
+# SIMT kernels: fp32 flops of the same contractions on CUDA cores ("alu");
+# delta pre-pass: bytes (hbm).
+def kernel_work(name: str, c: dict, out_bytes: int):
+    T, D = nominal_triples(c), c["D"]
+    rows = c["B"] * c["H"] * c["N"]
+    table = {
+        "tc_fwd": ("tensor", 4 * T * D),            # S = A K^T and U = P V
+        "tc_bwd_kv": ("tensor", 8 * T * D),         # S, dP recompute; dV += P A_dP; dK += dS A_S
+        "tc_bwd_q": ("tensor", 8 * T * D),          # S, dP recompute; W = dS K; U = P V
+        "simt_fwd": ("alu", 4 * T * D),
+        "simt_bwd_dq": ("alu", 6 * T * D),
+        "simt_bwd_dk2": ("alu", 8 * T * D),
+        "simt_bwd_dk": ("alu", 8 * T * D),
+        "simt_delta": ("hbm", rows * D * (2 + out_bytes) + rows * 4),
+        "tc_delta": ("hbm", rows * D * (2 + out_bytes) + rows * 4),
+    }
+    return table.get(name)
+
+
+def alu_peak_tflops(sm_mhz: float) -> float:
+    """fp32 FMA peak: 148 SMs x 128 FP32 lanes x 2 flop x clock."""
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [ln.split(",") for ln in open(self.f.name).read().strip().splitlines() if ln.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------------
+# Reference arm / cpu_baseline: the float64 oracle on a bounded, window-exact sample.
+# --------------------------------------------------------------------------------------------
+def oracle_sample(c, seed, L):
+    """Queries [a, a+L) of slice (b=0, h=0) with the (max(w1,w2)-1)-row key halo as prefix, so
+    every sampled row sees its full window: oracle fwd+bwd.  Returns (seconds, paper flops)."""
+    import numpy as np
+
+    import oracle
+    N, D, w1, w2 = c["N"], c["D"], c["w1"], c["w2"]
+    npf = max(w1, w2) - 1
+    a = min(N - L, max(npf, N // 2))
+    g = torch.Generator().manual_seed(seed)
+    shape_q, shape_k = (1, L, 1, D), (1, L + npf, 1, D)
+    dt = torch.float32 if c["dtype"] == "f32" else torch.bfloat16
+    t = {n: torch.randn(shape_k if n in ("k", "v", "k2", "v2") else shape_q, generator=g).to(dt).double().numpy()
+         for n in ("q", "k", "v", "k2", "v2", "dO")}
+    t0 = time.perf_counter()
+    oracle.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, det=c["det"], n_prefix=npf)
+    if c["bwd"]:
+        oracle.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], t["dO"], w1, w2, det=c["det"], n_prefix=npf)
+    dt_s = time.perf_counter() - t0
+    which = ("fwd", "bwd") if c["bwd"] else ("fwd",)
+    flops = sum(PAPER_FLOPS_PER_TRIPLE_D[w] for w in which) * L * w1 * w2 * D
+    del np, a
+    return dt_s, flops
+
+
+def calibrate_oracle_rows(c, target_s):
+    import oracle
+    oracle.build()
+    L0 = 32
+    t0, _ = oracle_sample(c, 0, L0)
+    L = int(min(c["N"] - 1, max(L0, L0 * target_s / max(t0, 1e-3))))
+    return L
+
+
+def cpu_baseline(c, target_s=15.0):
+    import oracle
+    L = calibrate_oracle_rows(c, target_s)
+    secs, flops = oracle_sample(c, 1, L)
+    return {"value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": oracle.threads_used(),
+            "kind": "oracle",
+            "sample": f"float64 C oracle, fwd+bwd of {L} query rows (b=0,h=0) with a "
+                      f"{max(c['w1'], c['w2']) - 1}-row key halo of config {c['name']}, {secs:.1f} s; "
+                      f"paper-formula FLOPs of the sample / wall time"}
+
+
+def run_reference(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    L = calibrate_oracle_rows(c, target_s=max(2.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(c, 2, L)
+    tot_s, tot_f = 0.0, 0.0
+    for s in range(args.steps):
+        secs, fl = oracle_sample(c, 3 + s, L)
+        tot_s += secs
+        tot_f += fl
+    val = tot_f / tot_s / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(c, args.gpus),
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": oracle.threads_used(), "kind": "oracle",
+                         "sample": f"each step: fwd+bwd of {L} query rows (b=0,h=0, full key halo) of "
+                                   f"config {c['name']}"},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(c, n):
+    return {"workload": f"{c['name']}: B={c['B']} H={c['H']} N={c['N']} D={c['D']} w1={c['w1']} w2={c['w2']} "
+                        f"{'det' if c['det'] else 'trilinear'} {'fwd+bwd' if c['bwd'] else 'fwd'} per GPU",
+            "B": c["B"], "H": c["H"], "N": c["N"], "D": c["D"], "w1": c["w1"], "w2": c["w2"],
+            "variant": "det" if c["det"] else "trilinear", "global_batch_heads": c["B"] * c["H"] * n,
+            "seq_len": c["N"], "parallelism": f"bh-sharded x{n}",
+            "l2": "inputs larger than L2 (no flush): %.0f MB of inputs per step" % (
+                6 * c["B"] * c["N"] * c["H"] * c["D"] * 2 / 1e6),
+            "flop_basis": "paper formula: fwd 6*NW*D + bwd 21*NW*D, NW = B*H*N*w1*w2"}
+
+
+# --------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--out-f32", action="store_true", help="write o/grads in fp32 (parity runs)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    c = dict(CONFIGS[args.config], name=args.config)
+
+    if args.impl == "reference":
+        run_reference(args, c)
+        return
+
+    import paper_2507_02754_b200 as sa
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus or (world == 1 and args.gpus == 1), "launch N>1 under torchrun"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    sa.load_library(build=(rank == 0))
+    if world > 1:
+        dist.barrier()
+    B, H, N, D, w1, w2, det = (c[k] for k in ("B", "H", "N", "D", "w1", "w2", "det"))
+    inp = make_inputs(B, N, H, D, seed_of(args.config, salt=rank), dtype=c["dtype"], device="cpu")
+    t = {n: x.to(dev) for n, x in inp.items()}
+    out_bytes = 4 if args.out_f32 else 2
+    ws = None
+    o = lse = None
+
+    def step():
+        nonlocal o, lse, ws
+        o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, det=det, out_f32=args.out_f32)
+        if c["bwd"]:
+            sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2, det=det,
+                        out_f32=args.out_f32, workspace=ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K full steps ----------------
+    clocks = ClockSampler(local)
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = sa.launch_count()
+    sa.profile_enable(True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    sa.profile_enable(False)
+    launches = sa.launch_count() - launches0
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    prof = sa.profile_read()
+    if dist:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    which = ("fwd", "bwd") if c["bwd"] else ("fwd",)
+    flops_step = paper_flops(c, which) * world
+    value = flops_step * args.steps / (ms / 1e3) / 1e12
+    mma_flops_step = sum(MMA_FLOPS_PER_TRIPLE_D[w] for w in which) * nominal_triples(c) * D * world
+
+    # ---------------- fwd-only and bwd-only timings (separate loops) ----------------
+    extra = {}
+    if c["bwd"]:
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        e[0].record(stream)
+        for _ in range(args.steps):
+            o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, det=det, out_f32=args.out_f32)
+        e[1].record(stream)
+        e[2].record(stream)
+        for _ in range(args.steps):
+            sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2, det=det,
+                        out_f32=args.out_f32)
+        e[3].record(stream)
+        torch.cuda.synchronize()
+        fms, bms = e[0].elapsed_time(e[1]) / args.steps, e[2].elapsed_time(e[3]) / args.steps
+        extra = {"fwd_tflops": paper_flops(c, ("fwd",)) * world / (fms / 1e3) / 1e12,
+                 "bwd_tflops": paper_flops(c, ("bwd",)) * world / (bms / 1e3) / 1e12,
+                 "fwd_ms": fms, "bwd_ms": bms}
+
+    pk, pk_src = peaks()
+    peak_sust = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    mma_tflops = mma_flops_step * args.steps / (ms / 1e3) / 1e12
+
+    # ---------------- roofline of the dominant kernel ----------------
+    roof = None
+    if prof:
+        dom = max(prof, key=lambda n: prof[n][0])
+        tot_ms, cnt = prof[dom]
+        avg_ms = tot_ms / cnt
+        w = kernel_work(dom, c, out_bytes)
+        step_share = tot_ms / ms if ms > 0 else None
+        if w is not None:
+            bound, amount = w
+            if bound == "tensor":
+                ach, unit, peak = amount / (avg_ms / 1e3) / 1e12, "TFLOP/s", peak_sust
+            elif bound == "hbm":
+                ach, unit, peak = amount / (avg_ms / 1e3) / 1e9, "GB/s", pk["hbm_gbs"]
+            else:
+                ach, unit = amount / (avg_ms / 1e3) / 1e12, "TFLOP/s"
+                peak = alu_peak_tflops(clk.get("sm_max_mhz") or 1965.0)
+            roof = {"bound": bound, "kernel": dom, "achieved": ach, "peak": peak, "unit": unit,
+                    "frac": ach / peak, "traffic": None, "avg_launch_ms": avg_ms, "launches": cnt,
+                    "share_of_step": step_share,
+                    "peak_source": (f"{pk_src} MEASURED_PEAKS.json bf16_tflops_sustained" if bound == "tensor"
+                                    else f"{pk_src} hbm_gbs" if bound == "hbm"
+                                    else "148 SM x 128 FP32 lanes x 2 x max SM clock")}
+        roof_kernels = {n: {"ms_total": v[0], "launches": v[1]} for n, v in prof.items()}
+    else:
+        roof_kernels = {}
+
+    # ---------------- end-to-end through the C ABI from pinned host buffers ----------------
+    e2e = None
+    if not args.no_e2e and c["bwd"]:
+        h_in = {n: x.pin_memory() for n, x in inp.items()}
+        od = torch.float32 if args.out_f32 else torch.bfloat16
+        h_out = {n: torch.empty(inp["q" if n in ("o", "dq") else "k"].shape, dtype=od).pin_memory()
+                 for n in ("o", "dq", "dk", "dv", "dk2", "dv2")}
+        h_out["lse"] = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
+        scratch = sa.host_step(h_in, h_out, w1, w2, det=det, out_f32=args.out_f32, device=dev)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        n_e2e = max(1, min(args.steps, 5))
+        for _ in range(n_e2e):
+            sa.host_step(h_in, h_out, w1, w2, det=det, out_f32=args.out_f32, scratch=scratch, device=dev)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ems = a0.elapsed_time(a1)
+        if dist:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": flops_step * n_e2e / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in h_in.values()) * world,
+               "d2h_bytes_per_step": sum(x.numel() * x.element_size() for x in h_out.values()) * world,
+               "ms_per_step": ems / n_e2e, "api": "simplicial_attn_host_step (pinned host buffers)"}
+        del scratch
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(c)
+        except Exception as ex:  # the baseline must never break the bench line
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        fwd_path = sa.fwd_path(B, H, N, D, w1, w2, det=det, out_f32=args.out_f32)
+        bwd_path = sa.bwd_path(B, H, N, D, w1, w2, det=det, out_f32=args.out_f32)
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "compute": "bf16 inputs; fp16 MMA operands, fp32 accumulate (tcgen05) / fp32 (SIMT)",
+            "data": "synthetic",
+            "config": config_block(c, world),
+            "mma_basis_tflops": mma_tflops,
+            "pct_bf16_peak_mma_basis": 100.0 * mma_tflops / (peak_sust * world),
+            "pct_bf16_peak_paper_basis": 100.0 * value / (peak_sust * world),
+            "paths": {"fwd": {1: "simt", 2: "tcgen05"}.get(fwd_path, fwd_path),
+                      "bwd": {1: "simt", 2: "tcgen05"}.get(bwd_path, bwd_path)},
+            **extra,
+            "roofline": roof, "kernels": roof_kernels,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "peaks": {"bf16_tflops": pk["bf16_tflops"], "bf16_tflops_sustained": peak_sust,
+                      "hbm_gbs": pk["hbm_gbs"], "source": pk_src},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

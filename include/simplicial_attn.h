@@ -119,6 +119,13 @@ int simplicial_attn_bwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t
 /* Total kernels this library has launched since it was loaded (for the bench's gpu_launches). */
 uint64_t simplicial_attn_launch_count(void);
 
+/* Per-kernel device timing for the bench's roofline: while enabled, every kernel launch is
+ * bracketed by CUDA events recorded on its own stream.  read() synchronises those events, writes
+ * up to max_kernels entries (name in 32-byte slots, summed milliseconds, launch count), clears the
+ * record and returns the number of distinct kernels. */
+void simplicial_attn_profile_enable(int on);
+int simplicial_attn_profile_read(char* names32, double* total_ms, int64_t* counts, int max_kernels);
+
 const char* simplicial_attn_status_string(sa_status s);
 
 /* Library build identifier (compile target and date), e.g. "sm_100a ...". */

@@ -8,4 +8,5 @@ fallback: every entry point raises if the CUDA library or a CUDA device is missi
 from .binding import (  # noqa: F401
     SA_FORCE_SIMT, SA_IN_F32, SA_OUT_F32, SA_VARIANT_DET, SA_PATH_SIMT, SA_PATH_TCGEN05,
     backward, bwd_path, forward, fwd_path, host_step, launch_count, lib, load_library,
+    profile_enable, profile_read,
 )

@@ -27,6 +27,7 @@ EXPORTS = (
     "simplicial_attn_bwd", "simplicial_attn_bwd_prefixed", "simplicial_attn_host_step_scratch_bytes",
     "simplicial_attn_host_step", "simplicial_attn_fwd_path", "simplicial_attn_bwd_path",
     "simplicial_attn_launch_count", "simplicial_attn_status_string", "simplicial_attn_version",
+    "simplicial_attn_profile_enable", "simplicial_attn_profile_read",
 )
 
 _lib = None
@@ -59,6 +60,9 @@ def load_library(build: bool = True):
         "simplicial_attn_launch_count": ([], ctypes.c_uint64),
         "simplicial_attn_status_string": ([ctypes.c_int], ctypes.c_char_p),
         "simplicial_attn_version": ([], ctypes.c_char_p),
+        "simplicial_attn_profile_enable": ([ctypes.c_int], None),
+        "simplicial_attn_profile_read": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_int64), ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -182,3 +186,21 @@ def bwd_path(B, H, N, D, w1, w2, dtype=torch.bfloat16, det=False, out_f32=False,
 
 def launch_count() -> int:
     return int(lib().simplicial_attn_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every library kernel launch with CUDA events on its stream (bench roofline)."""
+    lib().simplicial_attn_profile_enable(1 if on else 0)
+
+
+def profile_read(max_kernels: int = 64) -> dict:
+    """{kernel name: (total ms, launches)} recorded since the last read; clears the record."""
+    names = ctypes.create_string_buffer(32 * max_kernels)
+    tot = (ctypes.c_double * max_kernels)()
+    cnt = (ctypes.c_int64 * max_kernels)()
+    n = lib().simplicial_attn_profile_read(names, tot, cnt, max_kernels)
+    out = {}
+    for k in range(n):
+        nm = names.raw[32 * k:32 * k + 32].split(b"\0", 1)[0].decode()
+        out[nm] = (float(tot[k]), int(cnt[k]))
+    return out

@@ -1,7 +1,11 @@
 // sa_api.cu -- the C ABI (include/simplicial_attn.h): validation, kernel selection, launches.
 #include <atomic>
 #include <math.h>
+#include <mutex>
 #include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
 
 #include "sa_common.cuh"
 
@@ -9,6 +13,36 @@ namespace sa {
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(uint64_t(n), std::memory_order_relaxed); }
+
+// ---- per-kernel event timing (simplicial_attn_profile_*) ----
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::atomic<int> g_prof_on{0};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;
+
+KernelScope::KernelScope(const char* name, cudaStream_t s) : slot(-1), st(s) {
+  note_launch(1);
+  if (!g_prof_on.load(std::memory_order_relaxed)) return;
+  ProfRec r{name, nullptr, nullptr};
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  slot = int(g_prof.size());
+  g_prof.push_back(r);
+}
+KernelScope::~KernelScope() {
+  if (slot < 0) return;
+  cudaEvent_t e;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    e = g_prof[slot].b;
+  }
+  cudaEventRecord(e, st);
+}
 
 cudaError_t simt_forward(const Problem& p, bool in_f32, bool out_f32, const void* q, const void* k,
                          const void* v, const void* k2, const void* v2, void* o, float* lse, cudaStream_t st);
@@ -216,6 +250,39 @@ int simplicial_attn_bwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t
 }
 
 uint64_t simplicial_attn_launch_count(void) { return g_launches.load(); }
+
+void simplicial_attn_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+
+int simplicial_attn_profile_read(char* names32, double* total_ms, int64_t* counts, int max_kernels) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    recs.swap(g_prof);
+  }
+  std::vector<std::string> names;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto& r : recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+    size_t k = 0;
+    while (k < names.size() && names[k] != r.name) ++k;
+    if (k == names.size()) { names.push_back(r.name); tot.push_back(0); cnt.push_back(0); }
+    tot[k] += ms;
+    cnt[k] += 1;
+  }
+  int n = int(names.size()) < max_kernels ? int(names.size()) : max_kernels;
+  for (int k = 0; k < n; ++k) {
+    strncpy(names32 + 32 * k, names[k].c_str(), 31);
+    names32[32 * k + 31] = 0;
+    total_ms[k] = tot[k];
+    counts[k] = cnt[k];
+  }
+  return n;
+}
 
 const char* simplicial_attn_status_string(sa_status s) {
   switch (s) {

@@ -46,4 +46,12 @@ __host__ __device__ __forceinline__ int win_lo(int pos, int w) { return pos - w 
 // Launch bookkeeping (sa_api.cu).
 void note_launch(int n = 1);
 
+// Brackets one kernel launch with CUDA events on `st` while profiling is enabled (sa_api.cu).
+struct KernelScope {
+  KernelScope(const char* name, cudaStream_t st);
+  ~KernelScope();
+  int slot;
+  cudaStream_t st;
+};
+
 }  // namespace sa

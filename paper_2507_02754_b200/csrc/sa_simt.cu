@@ -369,9 +369,9 @@ template <typename TIn, typename TOut, int NV>
 cudaError_t launch_fwd_t(const Problem& p, const void* q, const void* k, const void* v, const void* k2,
                          const void* v2, void* o, float* lse, cudaStream_t st) {
   dim3 grid(p.N, p.B * p.H);
+  KernelScope ks("simt_fwd", st);
   simt_fwd<TIn, TOut, NV><<<grid, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
                                                       (const TIn*)k2, (const TIn*)v2, (TOut*)o, lse);
-  note_launch();
   return cudaGetLastError();
 }
 
@@ -380,19 +380,30 @@ cudaError_t launch_bwd_t(const Problem& p, const void* q, const void* k, const v
                          const void* v2, const void* o, const float* lse, const void* dO, void* dq,
                          void* dk, void* dv, void* dk2, void* dv2, float* delta, cudaStream_t st) {
   int64_t rows = int64_t(p.B) * p.H * p.N;
-  simt_delta<TIn, TOut><<<unsigned((rows + kWarps - 1) / kWarps), kThreads, 0, st>>>(
-      p, (const TIn*)dO, (const TOut*)o, delta);
+  {
+    KernelScope ks("simt_delta", st);
+    simt_delta<TIn, TOut><<<unsigned((rows + kWarps - 1) / kWarps), kThreads, 0, st>>>(
+        p, (const TIn*)dO, (const TOut*)o, delta);
+  }
   dim3 gq(p.N, p.B * p.H), gk(p.NK(), p.B * p.H);
-  simt_bwd_dq<TIn, TOut, NV><<<gq, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
-                                                       (const TIn*)k2, (const TIn*)v2, (const TIn*)dO,
-                                                       lse, delta, (TOut*)dq);
-  simt_bwd_dk2<TIn, TOut, NV><<<gk, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
-                                                        (const TIn*)k2, (const TIn*)v2, (const TIn*)dO,
-                                                        lse, delta, (TOut*)dk2, (TOut*)dv2);
-  simt_bwd_dk<TIn, TOut, NV><<<gk, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
-                                                       (const TIn*)k2, (const TIn*)v2, (const TIn*)dO,
-                                                       lse, delta, (TOut*)dk, (TOut*)dv);
-  note_launch(4);
+  {
+    KernelScope ks("simt_bwd_dq", st);
+    simt_bwd_dq<TIn, TOut, NV><<<gq, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
+                                                         (const TIn*)k2, (const TIn*)v2, (const TIn*)dO,
+                                                         lse, delta, (TOut*)dq);
+  }
+  {
+    KernelScope ks("simt_bwd_dk2", st);
+    simt_bwd_dk2<TIn, TOut, NV><<<gk, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
+                                                          (const TIn*)k2, (const TIn*)v2, (const TIn*)dO,
+                                                          lse, delta, (TOut*)dk2, (TOut*)dv2);
+  }
+  {
+    KernelScope ks("simt_bwd_dk", st);
+    simt_bwd_dk<TIn, TOut, NV><<<gk, kThreads, 0, st>>>(p, (const TIn*)q, (const TIn*)k, (const TIn*)v,
+                                                         (const TIn*)k2, (const TIn*)v2, (const TIn*)dO,
+                                                         lse, delta, (TOut*)dk, (TOut*)dv);
+  }
   return cudaGetLastError();
 }
 
