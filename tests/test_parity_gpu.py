@@ -108,6 +108,14 @@ def test_prefixed_mode(dtype, tol):
     assert_close(got, ref, tol)
 
 
+def test_tensor_core_path_selected():
+    """bf16 inputs with D in {64,128} and a folded window <= 128 must run the tcgen05 kernels."""
+    assert sa.fwd_path(4, 16, 8192, 128, 512, 32) == sa.SA_PATH_TCGEN05
+    assert sa.fwd_path(2, 16, 16384, 128, 512, 32, det=True) == sa.SA_PATH_TCGEN05
+    assert sa.fwd_path(1, 2, 256, 64, 16, 48) == sa.SA_PATH_TCGEN05
+    assert sa.fwd_path(1, 2, 256, 128, 512, 32, dtype=torch.float32) == sa.SA_PATH_SIMT
+
+
 def test_deterministic():
     inp = make_inputs(1, 300, 2, 128, seed=3, dtype="bf16")
     a = run_cuda(inp, 128, 32, False)
