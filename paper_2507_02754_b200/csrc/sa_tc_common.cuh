@@ -35,20 +35,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 10000000;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
-// Wait until the phase with the given parity has completed.  A wait longer than ~30 s (a
-// pipeline deadlock) traps, turning a hang into a reported launch failure.
+// Wait until the phase with the given parity has completed.  try_wait suspends the warp in
+// hardware (time hint 10 ms) instead of spinning on the issue slots; ~4000 expired hints
+// (a pipeline deadlock, tens of seconds) trap, turning a hang into a reported launch failure.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait(bar, parity)) return;
-  const long long t0 = clock64();
+  uint32_t n = 0;
+  long long t0 = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > 60000000000LL) __trap();
+    if (++n == 64u) t0 = clock64();
+    if (n > 64u && (n & 255u) == 0 && clock64() - t0 > 40000000000LL) __trap();
   }
 }
 

@@ -11,9 +11,10 @@
 // P:241-244).  K and V tiles arrive by TMA (128B swizzle) into a 3-stage ring; all MMAs use fp16
 // operands with fp32 accumulation (K/V converted from bf16 exactly by a pre-pass).
 //
-// Warp roles (256 threads, 1 CTA/SM, persistent over (b,h,tile) items):
+// Warp roles (384 threads, 1 CTA/SM, persistent over (b,h,tile) items):
 //   warp 0: TMA producer;  warp 1: TMEM allocator + single-thread MMA issuer;
-//   warps 4-7: row softmax + epilogue (warp w owns TMEM lanes 32(w-4)..32(w-4)+31).
+//   warps 4-11: row softmax + epilogue; warps 4+q and 8+q own TMEM lanes 32q..32q+31 and split
+//   each S chunk's columns in two halves (max exchanged through shared memory).
 #include <math.h>
 
 #include <algorithm>
@@ -31,7 +32,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int kStages = 3;
 constexpr int kChunk = 128;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -58,8 +59,9 @@ struct Smem {
   static constexpr int kStageBytes = kChunk * D * 2;
   alignas(1024) uint8_t k[kStages][kStageBytes];
   alignas(1024) uint8_t v[kStages][kStageBytes];
-  float ebuf[128][33];
-  float rm[128], rl[128];
+  float ebuf[2][128][17];
+  float xmax[2][2][128];
+  float rm[128], rl[2][128];
   float gM[128], gL[128];
   uint64_t kfull[kStages], kempty[kStages], vfull[kStages], vempty[kStages];
   uint64_t sfull[2], pready[2], pvdone, udone, aready;
@@ -110,11 +112,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.sfull[s], 1);
-      mbar_init(&sm.pready[s], 4);
+      mbar_init(&sm.pready[s], 8);
     }
     mbar_init(&sm.pvdone, 1);
     mbar_init(&sm.udone, 1);
-    mbar_init(&sm.aready, 4);
+    mbar_init(&sm.aready, 8);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
@@ -199,12 +201,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------ softmax + epilogue ------------------------------
-    const int qd = warp - 4;
+    // 8 warps: warp 4+qd and 8+qd share TMEM lane quadrant qd (rows r = 32 qd + lane); the
+    // first ("half 0") handles chunk columns [0,64), the second [64,128).
+    const int qd = warp & 3, half = (warp - 4) >> 2;
     const int r = qd * 32 + lane;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t tU = tbase + kColU + lane_off, tA = tbase + kColA + lane_off;
     const uint32_t tS[2] = {tbase + kColS0 + lane_off, tbase + kColS1 + lane_off};
     const Problem& p = a.p;
+    const int cbase = 64 * half;
+    constexpr int kUH = D / 2;  // U columns per half
     uint32_t cc = 0, pvc = 0, gc = 0;
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
       Item it = get_item(a, item);
@@ -227,8 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr int D3 = (D / 3) * 3;
 #pragma unroll
             for (int base = 0; base < D; base += 24) {
-              constexpr int kMax = 24;
-              float qf[kMax], kf[kMax], av[kMax];
+              float qf[24], kf[24], av[24];
 #pragma unroll
               for (int u = 0; u < 3; ++u) {
                 if (base + 8 * u < D) {
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
 #pragma unroll
-              for (int c3 = 0; c3 < kMax; c3 += 3) {
+              for (int c3 = 0; c3 < 24; c3 += 3) {
                 if (base + c3 + 3 <= D3) {
                   // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
                   av[c3 + 0] = kf[c3 + 1] * qf[c3 + 2] - kf[c3 + 2] * qf[c3 + 1];
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
 #pragma unroll
-              for (int e = 0; e < kMax; e += 2)
+              for (int e = 0; e < 24; e += 2)
                 if (base + e < D) pk[(base + e) / 2] = pack_f16x2(a.a_scale * av[e], a.a_scale * av[e + 1]);
             }
           } else {
@@ -275,46 +280,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-#pragma unroll
-        for (int t = 0; t < D / 64; ++t) tmem_st32(tA + 32 * t, *reinterpret_cast<uint32_t(*)[32]>(pk + 32 * t));
+        // each half stores its D/4 packed columns
+        if (D == 128) {
+          if (half == 0)
+            tmem_st32(tA, *reinterpret_cast<uint32_t(*)[32]>(pk));
+          else
+            tmem_st32(tA + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32 % (D / 2)));
+        } else {
+          if (half == 0)
+            tmem_st16(tA, pk);
+          else
+            tmem_st16(tA + 16, pk + 16 % (D / 2));
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.aready);
       }
 
-      // ---- chunks: per-row online softmax ----
+      // ---- chunks: per-row online softmax (conditional rescaling, FA4-style threshold) ----
       float m_ref = -INFINITY, l = 0.f;
       const int jlo = max(0, pos - p.w1 + 1);
       for (int c = 0; c < it.nch; ++c) {
         const uint32_t sb = (cc + c) & 1, ph = ((cc + c) >> 1) & 1;
         const int w = chunk_width(it, c);
+        const bool act = cbase < w;  // warp-uniform
+        const int nw = act ? min(64, w - cbase) : 0;
         mbar_wait(&sm.sfull[sb], ph);
         tc_fence_after();
-        float sv[kChunk];
-        {
+        float sv[64];
+        if (act) {
           uint32_t* su = reinterpret_cast<uint32_t*>(sv);
-#pragma unroll
-          for (int t = 0; t < kChunk / 32; ++t)
-            if (t * 32 < w) {
-              if (t * 32 + 16 >= w)
-                tmem_ld16(tS[sb] + 32 * t, su + 32 * t);
-              else
-                tmem_ld32(tS[sb] + 32 * t, *reinterpret_cast<uint32_t(*)[32]>(su + 32 * t));
-            }
+          if (nw == 64) {
+            tmem_ld32(tS[sb] + cbase, *reinterpret_cast<uint32_t(*)[32]>(su));
+            tmem_ld32(tS[sb] + cbase + 32, *reinterpret_cast<uint32_t(*)[32]>(su + 32));
+          } else {
+            if (nw >= 32) tmem_ld32(tS[sb] + cbase, *reinterpret_cast<uint32_t(*)[32]>(su));
+            if (nw == 16) tmem_ld16(tS[sb] + cbase, su);
+            if (nw == 48) tmem_ld16(tS[sb] + cbase + 32, su + 32);
+          }
           tmem_ld_wait();
         }
-        const int jc0 = it.jbeg + c * kChunk;
-        const int lo_rel = jlo - jc0, hi_rel = pos - jc0;
-        const bool need_mask = !valid || lo_rel > 0 || hi_rel < w - 1;
+        const int jc0 = it.jbeg + c * kChunk + cbase;
+        int lo_c = jlo - jc0, hi_c = min(pos - jc0, nw - 1);
+        if (!valid) { lo_c = 1; hi_c = 0; }
+        const bool need_mask = lo_c > 0 || hi_c < 63;
         float mx = -INFINITY;
+        if (act) {
+          if (!__any_sync(0xffffffffu, need_mask)) {
 #pragma unroll
-        for (int jj = 0; jj < kChunk; ++jj) {
-          if (jj < w) {
-            if (need_mask && (!valid || jj < lo_rel || jj > hi_rel)) sv[jj] = -INFINITY;
-            mx = fmaxf(mx, sv[jj]);
+            for (int jj = 0; jj < 64; ++jj) mx = fmaxf(mx, sv[jj]);
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 64; ++jj) {
+              sv[jj] = (jj >= lo_c && jj <= hi_c) ? sv[jj] : -INFINITY;
+              mx = fmaxf(mx, sv[jj]);
+            }
           }
         }
+        sm.xmax[c & 1][half][r] = mx;
+        named_bar_sync(1 + qd, 64);
+        mx = fmaxf(sm.xmax[c & 1][0][r], sm.xmax[c & 1][1][r]);
         if (c == 0) {
           m_ref = mx;
         } else {
@@ -325,13 +351,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const float alpha = need ? ex2(m_ref - mx) : 1.f;
 #pragma unroll
-            for (int t = 0; t < D / 32; ++t) {
+            for (int t = 0; t < kUH / 32; ++t) {
               uint32_t u[32];
-              tmem_ld32(tU + 32 * t, u);
+              tmem_ld32(tU + half * kUH + 32 * t, u);
               tmem_ld_wait();
 #pragma unroll
               for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * alpha);
-              tmem_st32(tU + 32 * t, u);
+              tmem_st32(tU + half * kUH + 32 * t, u);
             }
             tmem_st_wait();
             if (need) {
@@ -340,28 +366,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-        uint32_t pk[kChunk / 2];
-        float ls = 0.f;
+        if (act) {
+          const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
+          uint32_t pk[32];
+          float ls = 0.f;
 #pragma unroll
-        for (int t = 0; t < kChunk / 2; ++t) {
-          pk[t] = 0u;
-          if (2 * t < w) {
+          for (int t = 0; t < 32; ++t) {
             float p0 = ex2(sv[2 * t] - m_use), p1 = ex2(sv[2 * t + 1] - m_use);
             ls += p0 + p1;
             pk[t] = pack_f16x2(p0, p1);
           }
-        }
-        l += ls;
-#pragma unroll
-        for (int t = 0; t < kChunk / 64; ++t)
-          if (t * 64 < w) {
-            if (t * 64 + 32 >= w)
-              tmem_st16(tS[sb] + 32 * t, pk + 32 * t);
-            else
-              tmem_st32(tS[sb] + 32 * t, *reinterpret_cast<uint32_t(*)[32]>(pk + 32 * t));
+          // columns >= nw were masked to -inf above (need_mask is set whenever nw < 64)
+          l += ls;
+          const uint32_t pcol = tS[sb] + 32 * half;
+          if (nw == 64) {
+            tmem_st32(pcol, pk);
+          } else {
+            if (nw >= 32) tmem_st16(pcol, pk);
+            if (nw == 16) tmem_st8(pcol, pk);
+            if (nw == 48) tmem_st8(pcol + 16, pk + 16);
           }
-        tmem_st_wait();
+          tmem_st_wait();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pready[sb]);
@@ -370,34 +396,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- epilogue: merge the R rows of each query, v2 o U, normalise ----
       mbar_wait(&sm.udone, gc & 1);
       tc_fence_after();
-      sm.rm[r] = valid ? m_ref : -INFINITY;
-      sm.rl[r] = valid ? l : 0.f;
-      named_bar_sync(1, 128);
-      if (r < it.nq) {
+      if (half == 0) sm.rm[r] = valid ? m_ref : -INFINITY;
+      sm.rl[half][r] = valid ? l : 0.f;
+      named_bar_sync(5, 256);
+      if (half == 0 && r < it.nq) {
         float M = -INFINITY;
         for (int t = 0; t < a.R; ++t) M = fmaxf(M, sm.rm[r * a.R + t]);
         float L = 0.f;
         for (int t = 0; t < a.R; ++t) {
           float mt = sm.rm[r * a.R + t];
-          if (mt != -INFINITY) L += sm.rl[r * a.R + t] * ex2(mt - M);
+          if (mt != -INFINITY) L += (sm.rl[0][r * a.R + t] + sm.rl[1][r * a.R + t]) * ex2(mt - M);
         }
         sm.gM[r] = M;
         sm.gL[r] = L;
         a.lse[(int64_t(it.b) * p.H + it.h) * p.N + it.i0 + r] = (M + log2f(L)) * kLn2;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(5, 256);
       const float crow = (valid && m_ref != -INFINITY) ? ex2(m_ref - sm.gM[g]) : 0.f;
-      const __nv_bfloat16* v2row = a.v2 + p.koff(it.b, valid ? kpos : 0, it.h);
+      const __nv_bfloat16* v2row = a.v2 + p.koff(it.b, valid ? kpos : 0, it.h) + half * kUH;
+      float(*eb)[17] = sm.ebuf[half];
 #pragma unroll 1
-      for (int cb = 0; cb < D / 32; ++cb) {
-        uint32_t u[32];
-        tmem_ld32(tU + 32 * cb, u);
+      for (int cb = 0; cb < kUH / 16; ++cb) {
+        uint32_t u[16];
+        tmem_ld16(tU + half * kUH + 16 * cb, u);
         tmem_ld_wait();
-        float vv[32];
+        float vv[16];
         if (valid) {
-          const uint4* vp = reinterpret_cast<const uint4*>(v2row + 32 * cb);
+          const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
+          for (int t = 0; t < 2; ++t) {
             uint4 x = __ldg(vp + t);
             uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -409,23 +436,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) vv[e] = 0.f;
+          for (int e = 0; e < 16; ++e) vv[e] = 0.f;
         }
 #pragma unroll
-        for (int e = 0; e < 32; ++e) sm.ebuf[r][e] = crow * vv[e] * __uint_as_float(u[e]);
-        named_bar_sync(1, 128);
-        for (int idx = r; idx < it.nq * 32; idx += 128) {
-          const int gq = idx >> 5, d = idx & 31;
+        for (int e = 0; e < 16; ++e) eb[r][e] = crow * vv[e] * __uint_as_float(u[e]);
+        named_bar_sync(6 + half, 128);
+        for (int idx = r; idx < it.nq * 16; idx += 128) {
+          const int gq = idx >> 4, d = idx & 15;
           float s = 0.f;
-          for (int t = 0; t < a.R; ++t) s += sm.ebuf[gq * a.R + t][d];
+          for (int t = 0; t < a.R; ++t) s += eb[gq * a.R + t][d];
           const float val = s / sm.gL[gq];
-          const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + 32 * cb + d;
+          const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + half * kUH + 16 * cb + d;
           if (a.out_f32)
             reinterpret_cast<float*>(a.o)[off] = val;
           else
             reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(val);
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(6 + half, 128);
       }
       tc_fence_before();
       cc += it.nch;
