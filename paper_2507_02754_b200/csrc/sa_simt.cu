@@ -453,3 +453,31 @@ cudaError_t simt_backward(const Problem& p, bool in_f32, bool out_f32, const voi
 }
 
 }  // namespace sa
+
+namespace sa {
+// dk, dv only (CUDA-core kernel), given lse and delta; used by the tensor-core backward for
+// shapes its K/V-stationary kernel does not cover.
+cudaError_t simt_bwd_dk_only(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
+                             const void* k2, const void* v2, const void* dO, const float* lse, const float* delta,
+                             void* dk, void* dv, cudaStream_t st) {
+  using bf = __nv_bfloat16;
+  dim3 gk(p.NK(), p.B * p.H);
+  KernelScope ks("simt_bwd_dk", st);
+#define SA_DK_LAUNCH(NV)                                                                                       \
+  if (out_f32)                                                                                                 \
+    simt_bwd_dk<bf, float, NV><<<gk, kThreads, 0, st>>>(p, (const bf*)q, (const bf*)k, (const bf*)v,            \
+                                                        (const bf*)k2, (const bf*)v2, (const bf*)dO, lse, delta, \
+                                                        (float*)dk, (float*)dv);                                \
+  else                                                                                                         \
+    simt_bwd_dk<bf, bf, NV><<<gk, kThreads, 0, st>>>(p, (const bf*)q, (const bf*)k, (const bf*)v, (const bf*)k2, \
+                                                     (const bf*)v2, (const bf*)dO, lse, delta, (bf*)dk, (bf*)dv);
+  switch ((p.D + 31) / 32) {
+    case 1: SA_DK_LAUNCH(1) break;
+    case 2: SA_DK_LAUNCH(2) break;
+    case 3: SA_DK_LAUNCH(3) break;
+    default: SA_DK_LAUNCH(4) break;
+  }
+#undef SA_DK_LAUNCH
+  return cudaGetLastError();
+}
+}  // namespace sa

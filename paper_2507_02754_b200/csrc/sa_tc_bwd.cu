@@ -1,9 +1,655 @@
-// sa_tc_bwd.cu -- tcgen05/TMEM/TMA backward (bf16 inputs).  Placeholder until the kernels land.
-#include "sa_common.cuh"
+// sa_tc_bwd.cu -- tcgen05/TMEM/TMA backward of sliding-window 2-simplicial attention (bf16 in).
+//
+// Split as in the paper ("one kernel for dK and dV, another for dK', dV' and dQ"), with no
+// global atomics:
+//   delta  : delta_i = <dO_i, o_i>                                          (P:856 D_ptr)
+//   bwd_q  : rows (i,k) x j-chunks.  S = A_S K^T, dP = A_dP V^T (recompute, TS-MMA), then
+//            P = exp(S - lse_i), dS = P (dP - delta_i) on the CUDA cores, and
+//            W += dS K, U += P V (TS-MMA, fp32 in TMEM).  Epilogue:
+//              dq_i  = s sum_k k2_k o W_(i,k)        (det: W x k2_k)
+//              dk2_k = s sum_i q_i o W_(i,k)         (det: q_i x W)
+//              dv2_k =   sum_i dO_i o U_(i,k)
+//            dk2/dv2 rows are reduced across consecutive tiles in a shared-memory ring carried
+//            by each CTA over a contiguous tile range ("segment carry"); the w2-1 rows shared
+//            with the neighbouring range go to a small band workspace and are added by `fold`
+//            (deterministic replacement for the paper's even/odd two-stage launches, Alg. 2).
+//   bwd_kv : K/V-stationary; a CTA owns 128 key rows j of K and V (TMEM lanes = j) and walks
+//            the row tiles that touch them: S^T = K A_S^T, dP^T = V A_dP^T (SS-MMA), P^T and
+//            dS^T on the CUDA cores, dV += P^T A_dP, dK += dS^T A_S (TS-MMA).
+// Row operands: A_S = s (q o k2)  [det: s (k2 x q)],  A_dP = dO o v2, fp16; K, V fp16 copies.
+#include <math.h>
+
+#include <algorithm>
+#include <utility>
+
+#include "sa_tc_rows.cuh"
+
 namespace sa {
-bool tc_bwd_supported(const Problem&) { return false; }
-size_t tc_bwd_workspace_bytes(const Problem&) { return 0; }
-cudaError_t tc_backward(const Problem&, bool, const void*, const void*, const void*, const void*, const void*,
-                        const void*, const float*, const void*, void*, void*, void*, void*, void*, void*, size_t,
-                        cudaStream_t) { return cudaErrorNotSupported; }
+
+cudaError_t convert_pair_f16(const void* a, void* ao, const void* b, void* bo, int64_t n, int num_sms,
+                             cudaStream_t st);
+int num_sms();
+
+namespace {
+
+using namespace tc;
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMaxR = 64;  // bwd_q: rows per query (folded window w2) supported by the ring
+constexpr int kRingMax = 66;
+
+// ------------------------------------------------------------------------------------------
+// delta_i = <dO_i, o_i>, one warp per query row
+// ------------------------------------------------------------------------------------------
+template <typename TOut>
+__global__ void __launch_bounds__(256) delta_kernel(Problem p, const __nv_bfloat16* __restrict__ dO,
+                                                    const TOut* __restrict__ o, float* __restrict__ delta) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= int64_t(p.B) * p.H * p.N) return;
+  const int i = row % p.N, bh = row / p.N, b = bh / p.H, h = bh % p.H;
+  const __nv_bfloat16* g = dO + p.qoff(b, i, h);
+  const TOut* y = o + p.qoff(b, i, h);
+  float x = 0.f;
+  for (int d = lane; d < p.D; d += 32) x = fmaf(__bfloat162float(g[d]), ld_f(y + d), x);
+  x = warp_sum(x);
+  if (lane == 0) delta[row] = x;
+}
+
+// ==========================================================================================
+// bwd_q: dQ, dK2, dV2
+// ==========================================================================================
+constexpr int kQThreads = 384;
+constexpr int kQStages = 3;
+constexpr int kQChunk = 64;
+// TMEM columns
+constexpr uint32_t kQW = 0, kQU = 128, kQS = 256, kQdP = 320, kQAS = 384, kQAdP = 448;
+
+struct BwdQArgs {
+  Problem p;  // after the swap: w2 = R rows per query
+  const __nv_bfloat16 *q, *k2, *v2, *dO;
+  const float *lse, *delta;
+  void *dq, *dk2, *dv2;
+  float* band;  // [grid][2 start/end][2 k2/v2][R-1][D]
+  int out_f32, R, G, ngroups, items, per_cta, ring;
+};
+
+template <int D>
+struct QSmem {
+  static constexpr int kPanelBytes = kQChunk * 128;
+  static constexpr int kStageBytes = kQChunk * D * 2;
+  alignas(1024) uint8_t k[kQStages][kStageBytes];
+  alignas(1024) uint8_t v[kQStages][kStageBytes];
+  float acc_k2[kRingMax][D];
+  float acc_v2[kRingMax][D];
+  float eq[128][25], ek[128][25], ev[128][25];
+  uint64_t kvfull[kQStages], kvempty[kQStages];
+  uint64_t sfull, pready, udone, aready;
+  uint32_t tmem_base;
+};
+
+struct QItem {
+  int bh, b, h, grp, i0, nq, jbeg, span, nch;
+};
+
+__device__ __forceinline__ QItem q_item(const BwdQArgs& a, int item) {
+  QItem it;
+  it.bh = item / a.ngroups;
+  it.grp = item % a.ngroups;
+  it.b = it.bh / a.p.H;
+  it.h = it.bh % a.p.H;
+  it.i0 = it.grp * a.G;
+  it.nq = min(a.G, a.p.N - it.i0);
+  const int pos0 = a.p.np + it.i0, posl = pos0 + it.nq - 1;
+  it.jbeg = max(0, pos0 - a.p.w1 + 1);
+  it.span = posl - it.jbeg + 1;
+  it.nch = (it.span + kQChunk - 1) / kQChunk;
+  return it;
+}
+__device__ __forceinline__ int q_width(const QItem& it, int c) {
+  if (c < it.nch - 1) return kQChunk;
+  return ((it.span - kQChunk * (it.nch - 1)) + 15) & ~15;
+}
+
+// One epilogue pass over columns [c0, c0+PW) of the tile's W (half 0) / U (half 1) rows:
+// per-row contributions into eq/ek/ev, then reductions into dq (per query) and the dk2/dv2 ring.
+template <int D, int PW, bool DET>
+__device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a, const QItem& it, int c0, int half,
+                                                int r, bool valid, int g, int kpos, uint32_t tW, uint32_t tU,
+                                                int tid256) {
+  const Problem& p = a.p;
+  const float s = p.scale;
+  if (half == 0) {
+    float wv[PW], k2v[PW], qv[PW];
+    {
+      uint32_t u[PW];
+      if constexpr (PW >= 16) tmem_ld16(tW + c0, u);
+      if constexpr (PW == 24) tmem_ld8(tW + c0 + 16, u + 16);
+      if constexpr (PW == 8) tmem_ld8(tW + c0, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < PW; ++e) wv[e] = __uint_as_float(u[e]);
+    }
+    if (valid) {
+      load_bf16<PW>(a.k2 + p.koff(it.b, kpos, it.h) + c0, k2v);
+      load_bf16<PW>(a.q + p.qoff(it.b, it.i0 + g, it.h) + c0, qv);
+    } else {
+#pragma unroll
+      for (int e = 0; e < PW; ++e) k2v[e] = qv[e] = 0.f;
+    }
+    if (DET) {
+      constexpr int D3 = (D / 3) * 3;
+#pragma unroll
+      for (int t = 0; t < PW; t += 3) {
+        if (t + 3 <= PW && c0 + t + 3 <= D3) {
+          // dq: W x k2 ; dk2: q x W     ((x cross y)_r = x_{r+1} y_{r+2} - x_{r+2} y_{r+1})
+          sm.eq[r][t + 0] = s * (wv[t + 1] * k2v[t + 2] - wv[t + 2] * k2v[t + 1]);
+          sm.eq[r][t + 1] = s * (wv[t + 2] * k2v[t + 0] - wv[t + 0] * k2v[t + 2]);
+          sm.eq[r][t + 2] = s * (wv[t + 0] * k2v[t + 1] - wv[t + 1] * k2v[t + 0]);
+          sm.ek[r][t + 0] = s * (qv[t + 1] * wv[t + 2] - qv[t + 2] * wv[t + 1]);
+          sm.ek[r][t + 1] = s * (qv[t + 2] * wv[t + 0] - qv[t + 0] * wv[t + 2]);
+          sm.ek[r][t + 2] = s * (qv[t + 0] * wv[t + 1] - qv[t + 1] * wv[t + 0]);
+        } else {
+#pragma unroll
+          for (int e = t; e < t + 3 && e < PW; ++e) sm.eq[r][e] = sm.ek[r][e] = 0.f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < PW; ++e) {
+        sm.eq[r][e] = s * k2v[e] * wv[e];
+        sm.ek[r][e] = s * qv[e] * wv[e];
+      }
+    }
+  } else {
+    float uv[PW], dov[PW];
+    {
+      uint32_t u[PW];
+      if constexpr (PW >= 16) tmem_ld16(tU + c0, u);
+      if constexpr (PW == 24) tmem_ld8(tU + c0 + 16, u + 16);
+      if constexpr (PW == 8) tmem_ld8(tU + c0, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < PW; ++e) uv[e] = __uint_as_float(u[e]);
+    }
+    if (valid) {
+      load_bf16<PW>(a.dO + p.qoff(it.b, it.i0 + g, it.h) + c0, dov);
+    } else {
+#pragma unroll
+      for (int e = 0; e < PW; ++e) dov[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < PW; ++e) sm.ev[r][e] = dov[e] * uv[e];
+  }
+  named_bar_sync(1, 256);
+  // dq: sum over the R rows of each query
+  for (int idx = tid256; idx < it.nq * PW; idx += 256) {
+    const int gq = idx / PW, d = idx % PW;
+    float x = 0.f;
+    for (int t = 0; t < a.R; ++t) x += sm.eq[gq * a.R + t][d];
+    const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + d;
+    if (a.out_f32)
+      reinterpret_cast<float*>(a.dq)[off] = x;
+    else
+      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(x);
+  }
+  // dk2 / dv2: key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g)
+  const int P0 = p.np + it.i0;
+  const int nsl = a.R + it.nq - 1;
+  for (int idx = tid256; idx < nsl * PW; idx += 256) {
+    const int sl = idx / PW, d = idx % PW;
+    const int kp = P0 - a.R + 1 + sl;
+    if (kp < 0) continue;
+    float xk = 0.f, xv = 0.f;
+    const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
+    for (int gg = glo; gg <= ghi; ++gg) {
+      const int row = gg * a.R + (sl - gg);
+      xk += sm.ek[row][d];
+      xv += sm.ev[row][d];
+    }
+    const int slot = kp % a.ring;
+    sm.acc_k2[slot][c0 + d] += xk;
+    sm.acc_v2[slot][c0 + d] += xv;
+  }
+  named_bar_sync(1, 256);
+}
+
+template <int D, bool DET>
+__global__ void __launch_bounds__(kQThreads, 1)
+    tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  static_assert(sizeof(QSmem<D>) + 1024 <= 232448, "shared memory budget");
+  QSmem<D>& sm = *reinterpret_cast<QSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kPanels = D / 64;
+  constexpr uint32_t kPanelBytes = QSmem<D>::kPanelBytes;
+  const int it_begin = blockIdx.x * a.per_cta;
+  const int it_end = min(a.items, it_begin + a.per_cta);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(&sm.kvfull[s], 1);
+      mbar_init(&sm.kvempty[s], 1);
+    }
+    mbar_init(&sm.sfull, 1);
+    mbar_init(&sm.pready, 8);
+    mbar_init(&sm.udone, 1);
+    mbar_init(&sm.aready, 8);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  for (int e = threadIdx.x; e < kRingMax * D; e += kQThreads) {
+    (&sm.acc_k2[0][0])[e] = 0.f;
+    (&sm.acc_v2[0][0])[e] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      uint32_t kc = 0;
+      for (int item = it_begin; item < it_end; ++item) {
+        QItem it = q_item(a, item);
+        for (int c = 0; c < it.nch; ++c, ++kc) {
+          const int s = kc % kQStages;
+          const uint32_t ph = (kc / kQStages) & 1;
+          const int row = it.jbeg + c * kQChunk;
+          mbar_wait(&sm.kvempty[s], ph ^ 1);
+          mbar_expect_tx(&sm.kvfull[s], 2 * QSmem<D>::kStageBytes);
+          for (int pn = 0; pn < kPanels; ++pn) {
+            tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.h, row, it.b);
+            tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.h, row, it.b);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer ------------------------------
+    if (lane == 0) {
+      const uint32_t tW = tbase + kQW, tU = tbase + kQU, tS = tbase + kQS, tdP = tbase + kQdP;
+      const uint32_t tAS = tbase + kQAS, tAdP = tbase + kQAdP;
+      const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
+      uint32_t kc = 0, gc = 0;
+      for (int item = it_begin; item < it_end; ++item) {
+        QItem it = q_item(a, item);
+        mbar_wait(&sm.aready, gc & 1);
+        tc_fence_after();
+        for (int c = 0; c < it.nch; ++c) {
+          const int s = (kc + c) % kQStages;
+          const uint32_t ph = ((kc + c) / kQStages) & 1;
+          const int w = q_width(it, c);
+          mbar_wait(&sm.kvfull[s], ph);
+          tc_fence_after();
+          const uint32_t idesc_s = idesc_f16(128, w, 0, 0);
+          const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+            mma_ts(tS, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            mma_ts(tdP, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.sfull);
+          mbar_wait(&sm.pready, (kc + c) & 1);
+          tc_fence_after();
+          for (int kk = 0; kk < w / 16; ++kk) {
+            const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+            mma_ts(tW, tdP + kk * 8, smem_desc_sw128(kaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+            mma_ts(tU, tS + kk * 8, smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+          }
+          mma_commit(&sm.kvempty[s]);
+        }
+        mma_commit(&sm.udone);
+        kc += it.nch;
+        ++gc;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------ softmax-gradient + epilogue ------------------------------
+    const int qd = warp & 3, half = (warp - 4) >> 2;
+    const int r = qd * 32 + lane;
+    const int tid256 = threadIdx.x - 128;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t tW = tbase + kQW + lane_off, tU = tbase + kQU + lane_off;
+    const uint32_t tS = tbase + kQS + lane_off, tdP = tbase + kQdP + lane_off;
+    const uint32_t tAS = tbase + kQAS + lane_off, tAdP = tbase + kQAdP + lane_off;
+    const Problem& p = a.p;
+    uint32_t kc = 0, gc = 0;
+    int PS = 0, flush_lo = 0;
+    for (int item = it_begin; item < it_end; ++item) {
+      QItem it = q_item(a, item);
+      const bool first_in_sub = item == it_begin || it.grp == 0;
+      const bool last_in_sub = item == it_end - 1 || it.grp == a.ngroups - 1;
+      const int P0 = p.np + it.i0;
+      if (first_in_sub) {
+        PS = P0;
+        flush_lo = P0 - a.R + 1;
+      }
+      const int g = r / a.R, kk = r % a.R;
+      const bool row_in = r < a.G * a.R && g < it.nq;
+      const int pos = P0 + g;
+      const int kpos = pos - a.R + 1 + kk;
+      const bool valid = row_in && kpos >= 0;
+      float lse_l2 = 0.f, dl = 0.f;
+      if (row_in) {
+        const int64_t ri = (int64_t(it.b) * p.H + it.h) * p.N + it.i0 + g;
+        lse_l2 = a.lse[ri] * kLog2e;
+        dl = a.delta[ri];
+      }
+      // ---- row operands: half 0 -> A_S = s (q o k2) [det: s (k2 x q)], half 1 -> A_dP = dO o v2 ----
+      {
+        uint32_t pk[D / 2];
+#pragma unroll
+        for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
+        if (valid) {
+          if (half == 0)
+            row_operand_f16<D>(a.q + p.qoff(it.b, it.i0 + g, it.h), a.k2 + p.koff(it.b, kpos, it.h), p.scale, DET,
+                               pk);
+          else
+            row_operand_f16<D>(a.dO + p.qoff(it.b, it.i0 + g, it.h), a.v2 + p.koff(it.b, kpos, it.h), 1.f, false,
+                               pk);
+        }
+        tmem_store_row<D>(half == 0 ? tAS : tAdP, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.aready);
+      }
+      // ---- chunks: P = exp(S - lse), dS = P (dP - delta) ----
+      const int jlo = max(0, pos - p.w1 + 1);
+      for (int c = 0; c < it.nch; ++c) {
+        const int w = q_width(it, c);
+        const int cb = 32 * half;
+        const int nw = max(0, min(32, w - cb));
+        mbar_wait(&sm.sfull, (kc + c) & 1);
+        tc_fence_after();
+        if (nw > 0) {
+          uint32_t su[32], du[32];
+          if (nw == 32) {
+            tmem_ld32(tS + cb, su);
+            tmem_ld32(tdP + cb, du);
+          } else {
+            tmem_ld16(tS + cb, su);
+            tmem_ld16(tdP + cb, du);
+          }
+          tmem_ld_wait();
+          const int jc0 = it.jbeg + c * kQChunk + cb;
+          int lo_c = jlo - jc0, hi_c = min(pos - jc0, nw - 1);
+          if (!valid) {
+            lo_c = 1;
+            hi_c = 0;
+          }
+          const bool need_mask = lo_c > 0 || hi_c < 31;
+          uint32_t pp[16], pd[16];
+          if (!__any_sync(0xffffffffu, need_mask)) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), kLog2e, -lse_l2));
+              const float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), kLog2e, -lse_l2));
+              pp[t] = pack_f16x2(p0, p1);
+              pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), kLog2e, -lse_l2));
+              float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), kLog2e, -lse_l2));
+              p0 = (2 * t >= lo_c && 2 * t <= hi_c) ? p0 : 0.f;
+              p1 = (2 * t + 1 >= lo_c && 2 * t + 1 <= hi_c) ? p1 : 0.f;
+              pp[t] = pack_f16x2(p0, p1);
+              pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
+            }
+          }
+          if (nw == 32) {
+            tmem_st16(tS + 16 * half, pp);
+            tmem_st16(tdP + 16 * half, pd);
+          } else {
+            tmem_st8(tS + 16 * half, pp);
+            tmem_st8(tdP + 16 * half, pd);
+          }
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pready);
+      }
+      // ---- epilogue ----
+      mbar_wait(&sm.udone, gc & 1);
+      tc_fence_after();
+      if (DET) {
+#pragma unroll 1
+        for (int c0 = 0; c0 + 24 <= D; c0 += 24)
+          q_epilogue_pass<D, 24, DET>(sm, a, it, c0, half, r, valid, g, kpos, tW, tU, tid256);
+        if constexpr (D % 24 != 0)
+          q_epilogue_pass<D, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, g, kpos, tW, tU, tid256);
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 16)
+          q_epilogue_pass<D, 16, DET>(sm, a, it, c0, half, r, valid, g, kpos, tW, tU, tid256);
+      }
+      tc_fence_before();
+      // ---- flush ring rows that no later tile of this sub-range touches ----
+      const int PE = P0 + it.nq;
+      const int flush_hi = last_in_sub ? PE - 1 : P0 + a.G - a.R;  // inclusive
+      const bool end_open = last_in_sub && PE < p.np + p.N;
+      const bool start_open = PS > p.np;
+      const int nrows = flush_hi - flush_lo + 1;
+      for (int idx = tid256; idx < nrows * D; idx += 256) {
+        const int kp = flush_lo + idx / D, d = idx % D;
+        if (kp < 0 || kp >= p.NK()) continue;
+        const int slot = kp % a.ring;
+        const float vk = sm.acc_k2[slot][d], vv = sm.acc_v2[slot][d];
+        sm.acc_k2[slot][d] = 0.f;
+        sm.acc_v2[slot][d] = 0.f;
+        if (start_open && kp < PS) {
+          float* bnd = a.band + ((size_t(blockIdx.x) * 2 + 0) * 2) * (a.R - 1) * D;
+          const int rr = kp - (PS - a.R + 1);
+          bnd[size_t(rr) * D + d] = vk;
+          bnd[size_t(a.R - 1 + rr) * D + d] = vv;
+        } else if (end_open && kp + a.R - 1 >= PE) {
+          float* bnd = a.band + ((size_t(blockIdx.x) * 2 + 1) * 2) * (a.R - 1) * D;
+          const int rr = kp - (PE - a.R + 1);
+          bnd[size_t(rr) * D + d] = vk;
+          bnd[size_t(a.R - 1 + rr) * D + d] = vv;
+        } else {
+          const int64_t off = p.koff(it.b, kp, it.h) + d;
+          if (a.out_f32) {
+            reinterpret_cast<float*>(a.dk2)[off] = vk;
+            reinterpret_cast<float*>(a.dv2)[off] = vv;
+          } else {
+            reinterpret_cast<__nv_bfloat16*>(a.dk2)[off] = __float2bfloat16_rn(vk);
+            reinterpret_cast<__nv_bfloat16*>(a.dv2)[off] = __float2bfloat16_rn(vv);
+          }
+        }
+      }
+      flush_lo = flush_hi + 1;
+      named_bar_sync(1, 256);
+      kc += it.nch;
+      ++gc;
+    }
+  }
+
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_free<512>(tbase);
+}
+
+// Band fold: key rows shared by two consecutive CTA ranges get both partial sums; prefix rows no
+// query touches are zeroed.  One block per boundary (CTA c >= 1), plus a zeroing grid-stride.
+template <typename TOut>
+__global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
+  const Problem& p = a.p;
+  const int D = p.D, Rm1 = a.R - 1;
+  const int c = blockIdx.x + 1;
+  if (c < grid_q) {
+    const int item = c * a.per_cta;
+    if (item < a.items && (item % a.ngroups) != 0 && Rm1 > 0) {
+      const int bh = item / a.ngroups, b = bh / p.H, h = bh % p.H;
+      const int PS = p.np + (item % a.ngroups) * a.G;
+      const float* left = a.band + ((size_t(c - 1) * 2 + 1) * 2) * Rm1 * D;
+      const float* right = a.band + ((size_t(c) * 2 + 0) * 2) * Rm1 * D;
+      for (int idx = threadIdx.x; idx < Rm1 * D; idx += blockDim.x) {
+        const int rr = idx / D, d = idx % D;
+        const int kp = PS - a.R + 1 + rr;
+        if (kp < 0) continue;
+        const int64_t off = p.koff(b, kp, h) + d;
+        st_f(reinterpret_cast<TOut*>(a.dk2) + off, left[idx] + right[idx]);
+        st_f(reinterpret_cast<TOut*>(a.dv2) + off, left[size_t(Rm1) * D + idx] + right[size_t(Rm1) * D + idx]);
+      }
+    }
+  }
+  // prefix rows [0, np - R + 1) are outside every query's window: zero
+  const int nz = p.np - a.R + 1;
+  if (nz > 0) {
+    const int64_t total = int64_t(p.B) * p.H * nz * D;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+      const int d = e % D;
+      const int64_t t = e / D;
+      const int kp = t % nz, bh = t / nz, b = bh / p.H, h = bh % p.H;
+      const int64_t off = p.koff(b, kp, h) + d;
+      st_f(reinterpret_cast<TOut*>(a.dk2) + off, 0.f);
+      st_f(reinterpret_cast<TOut*>(a.dv2) + off, 0.f);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t simt_bwd_dk_only(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
+                             const void* k2, const void* v2, const void* dO, const float* lse, const float* delta,
+                             void* dk, void* dv, cudaStream_t st);
+
+static bool swapped(const Problem& p) { return p.w1 < p.w2; }
+
+bool tc_bwd_supported(const Problem& p) {
+  const int R = swapped(p) ? p.w1 : p.w2;
+  if (!(p.D == 64 || p.D == 128)) return false;
+  if (R < 2 || R > kMaxR) return false;
+  const int G = 128 / R;
+  return R + G <= kRingMax;
+}
+
+static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int q_grid(const Problem& p, int R, int G, int* per_cta, int* items_out) {
+  const int ngroups = (p.N + G - 1) / G;
+  const int items = ngroups * p.B * p.H;
+  const int min_tiles = (R + G - 1) / G + 1;  // a range must span >= R queries (band logic)
+  int grid = num_sms();
+  int pc = (items + grid - 1) / grid;
+  if (pc < min_tiles) pc = min_tiles;
+  grid = (items + pc - 1) / pc;
+  *per_cta = pc;
+  *items_out = items;
+  return grid;
+}
+
+size_t tc_bwd_workspace_bytes(const Problem& p0) {
+  Problem p = p0;
+  if (swapped(p)) std::swap(p.w1, p.w2);
+  const int R = p.w2, G = 128 / R;
+  int pc, items;
+  const int grid = q_grid(p, R, G, &pc, &items);
+  const size_t n = size_t(p.B) * p.NK() * p.H * p.D;
+  return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 2 * a256(n * 2) +
+         a256(sizeof(float) * size_t(grid) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
+}
+
+cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const void* k, const void* v, const void* k2,
+                        const void* v2, const void* o, const float* lse, const void* dO, void* dq, void* dk, void* dv,
+                        void* dk2, void* dv2, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Problem p = p0;
+  if (swapped(p)) {  // fold the smaller-window key into the query; gradients swap with it
+    std::swap(k, k2);
+    std::swap(v, v2);
+    std::swap(dk, dk2);
+    std::swap(dv, dv2);
+    std::swap(p.w1, p.w2);
+    if (p.det) p.scale = -p.scale;
+  }
+  if (ws_bytes < tc_bwd_workspace_bytes(p0)) return cudaErrorInvalidValue;
+  const int R = p.w2, G = 128 / R;
+  const size_t n = size_t(p.B) * p.NK() * p.H * p.D;
+  char* w = (char*)ws;
+  float* delta = (float*)w;
+  w += a256(sizeof(float) * size_t(p.B) * p.H * p.N);
+  char* kf = w;
+  w += a256(n * 2);
+  char* vf = w;
+  w += a256(n * 2);
+  float* band = (float*)w;
+
+  // delta
+  {
+    const int64_t rows = int64_t(p.B) * p.H * p.N;
+    KernelScope ks("tc_delta", st);
+    if (out_f32)
+      delta_kernel<float><<<unsigned((rows + 7) / 8), 256, 0, st>>>(p, (const __nv_bfloat16*)dO, (const float*)o, delta);
+    else
+      delta_kernel<__nv_bfloat16><<<unsigned((rows + 7) / 8), 256, 0, st>>>(p, (const __nv_bfloat16*)dO,
+                                                                             (const __nv_bfloat16*)o, delta);
+  }
+  cudaError_t e = convert_pair_f16(k, kf, v, vf, int64_t(n), num_sms(), st);
+  if (e != cudaSuccess) return e;
+
+  // bwd_q: dq, dk2, dv2
+  {
+    CUtensorMap tmK, tmV;
+    if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.H, p.D, kQChunk) ||
+        !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.H, p.D, kQChunk))
+      return cudaErrorInvalidValue;
+    BwdQArgs a;
+    a.p = p;
+    a.q = (const __nv_bfloat16*)q;
+    a.k2 = (const __nv_bfloat16*)k2;
+    a.v2 = (const __nv_bfloat16*)v2;
+    a.dO = (const __nv_bfloat16*)dO;
+    a.lse = lse;
+    a.delta = delta;
+    a.dq = dq;
+    a.dk2 = dk2;
+    a.dv2 = dv2;
+    a.band = band;
+    a.out_f32 = out_f32 ? 1 : 0;
+    a.R = R;
+    a.G = G;
+    a.ngroups = (p.N + G - 1) / G;
+    a.ring = R + G;
+    const int grid = q_grid(p, R, G, &a.per_cta, &a.items);
+    auto launch = [&](auto kern, size_t smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      KernelScope ks("tc_bwd_q", st);
+      kern<<<grid, kQThreads, smem, st>>>(tmK, tmV, a);
+    };
+    if (p.D == 128) {
+      if (p.det)
+        launch(tc_bwd_q_kernel<128, true>, sizeof(QSmem<128>) + 1024);
+      else
+        launch(tc_bwd_q_kernel<128, false>, sizeof(QSmem<128>) + 1024);
+    } else {
+      if (p.det)
+        launch(tc_bwd_q_kernel<64, true>, sizeof(QSmem<64>) + 1024);
+      else
+        launch(tc_bwd_q_kernel<64, false>, sizeof(QSmem<64>) + 1024);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    KernelScope ks("tc_fold", st);
+    const int fb = std::max(1, grid - 1);
+    if (out_f32)
+      fold_kernel<float><<<fb, 256, 0, st>>>(a, grid);
+    else
+      fold_kernel<__nv_bfloat16><<<fb, 256, 0, st>>>(a, grid);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  // bwd_kv: dk, dv (bring-up: CUDA-core kernel)
+  return simt_bwd_dk_only(p, out_f32, q, k, v, k2, v2, dO, lse, delta, dk, dv, st);
+}
+
 }  // namespace sa

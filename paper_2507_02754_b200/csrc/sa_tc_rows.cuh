@@ -1,0 +1,96 @@
+// sa_tc_rows.cuh -- per-row operand formation shared by the tensor-core kernels.
+//
+// An (i,k) row operand is a D-vector formed on the CUDA cores from two bf16 rows x, y:
+//   trilinear:   scale * (x o y)                      (a_(i,k) = s q_i o k2_k;  dO_i o v2_k)
+//   determinant: scale * (y x x) chunkwise over 3-dims (a_(i,k) = s k2_k x q_i, P:298-301;
+//                trailing D mod 3 dims are 0, reading R5)
+// packed as fp16x2 (low half = even element), the layout the K-major A operand takes in TMEM
+// (one row per TMEM lane, 2 elements per 32-bit column).
+#pragma once
+#include "sa_tc_common.cuh"
+
+namespace sa {
+namespace tc {
+
+template <int D>
+__device__ __forceinline__ void row_operand_f16(const __nv_bfloat16* x, const __nv_bfloat16* y, float scale,
+                                                bool cross, uint32_t (&pk)[D / 2]) {
+  const uint4* xp = reinterpret_cast<const uint4*>(x);
+  const uint4* yp = reinterpret_cast<const uint4*>(y);
+  if (cross) {
+    constexpr int D3 = (D / 3) * 3;
+#pragma unroll
+    for (int base = 0; base < D; base += 24) {
+      float xf[24], yf[24], av[24];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        if (base + 8 * u < D) {
+          uint4 a = __ldg(xp + base / 8 + u), b = __ldg(yp + base / 8 + u);
+          uint32_t as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 fa = bf16x2_to_f2(as[e]), fb = bf16x2_to_f2(bs[e]);
+            xf[8 * u + 2 * e] = fa.x;
+            xf[8 * u + 2 * e + 1] = fa.y;
+            yf[8 * u + 2 * e] = fb.x;
+            yf[8 * u + 2 * e + 1] = fb.y;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int c3 = 0; c3 < 24; c3 += 3) {
+        if (base + c3 + 3 <= D3) {  // (y x x)_r = y_{r+1} x_{r+2} - y_{r+2} x_{r+1}
+          av[c3 + 0] = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+          av[c3 + 1] = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+          av[c3 + 2] = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+        } else {
+          av[c3 + 0] = av[c3 + 1] = av[c3 + 2] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 24; e += 2)
+        if (base + e < D) pk[(base + e) / 2] = pack_f16x2(scale * av[e], scale * av[e + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < D / 8; ++t) {
+      uint4 a = __ldg(xp + t), b = __ldg(yp + t);
+      uint32_t as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 fa = bf16x2_to_f2(as[e]), fb = bf16x2_to_f2(bs[e]);
+        pk[4 * t + e] = pack_f16x2(scale * fa.x * fb.x, scale * fa.y * fb.y);
+      }
+    }
+  }
+}
+
+// Store a full packed row (D/2 columns) to TMEM at column address taddr (this warp's lanes).
+template <int D>
+__device__ __forceinline__ void tmem_store_row(uint32_t taddr, const uint32_t (&pk)[D / 2]) {
+#pragma unroll
+  for (int t = 0; t < D / 64; ++t) tmem_st32(taddr + 32 * t, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32 * t));
+}
+
+// Load n (<=32, multiple of 8) bf16 values starting at p (16B aligned) as floats.
+template <int N>
+__device__ __forceinline__ void load_bf16(const __nv_bfloat16* p, float (&f)[N]) {
+  const uint4* vp = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int t = 0; t < N / 8; ++t) {
+    uint4 x = __ldg(vp + t);
+    uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 g = bf16x2_to_f2(xs[e]);
+      f[8 * t + 2 * e] = g.x;
+      f[8 * t + 2 * e + 1] = g.y;
+    }
+  }
+}
+
+}  // namespace tc
+}  // namespace sa
