@@ -78,9 +78,13 @@ sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void*
                                        int64_t N, int64_t D, int64_t w1, int64_t w2,
                                        int64_t n_prefix, uint32_t flags, void* stream);
 
-/* Bytes of device workspace the backward needs (delta_i [B,H,N] fp32 plus kernel scratch). */
+/* Bytes of device workspace the backward needs (delta_i [B,H,N] fp32, fp16 copies of the
+ * key-side operands, band partials).  The _prefixed form sizes it for n_prefix halo rows. */
 size_t simplicial_attn_bwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
                                            int64_t w2, uint32_t flags);
+size_t simplicial_attn_bwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D,
+                                                    int64_t w1, int64_t w2, int64_t n_prefix,
+                                                    uint32_t flags);
 
 /* Backward.  Reads o (output dtype) and lse from the forward; writes dq [B,N,H,D] and
  * dk, dv, dk2, dv2 over all n_prefix+N key rows (rows no query touches are written as 0). */

@@ -24,6 +24,7 @@ _STATUS = {0: "SA_OK", 1: "SA_ERR_INVALID_ARG", 2: "SA_ERR_UNSUPPORTED", 3: "SA_
            4: "SA_ERR_CUDA"}
 EXPORTS = (
     "simplicial_attn_fwd", "simplicial_attn_fwd_prefixed", "simplicial_attn_bwd_workspace_bytes",
+    "simplicial_attn_bwd_workspace_bytes_prefixed",
     "simplicial_attn_bwd", "simplicial_attn_bwd_prefixed", "simplicial_attn_host_step_scratch_bytes",
     "simplicial_attn_host_step", "simplicial_attn_fwd_path", "simplicial_attn_bwd_path",
     "simplicial_attn_launch_count", "simplicial_attn_status_string", "simplicial_attn_version",
@@ -51,6 +52,7 @@ def load_library(build: bool = True):
         "simplicial_attn_fwd": ([P] * 7 + [I] * 6 + [U, P], ctypes.c_int),
         "simplicial_attn_fwd_prefixed": ([P] * 7 + [I] * 7 + [U, P], ctypes.c_int),
         "simplicial_attn_bwd_workspace_bytes": ([I] * 6 + [U], S),
+        "simplicial_attn_bwd_workspace_bytes_prefixed": ([I] * 7 + [U], S),
         "simplicial_attn_bwd": ([P] * 14 + [S] + [I] * 6 + [U, P], ctypes.c_int),
         "simplicial_attn_bwd_prefixed": ([P] * 14 + [S] + [I] * 7 + [U, P], ctypes.c_int),
         "simplicial_attn_host_step_scratch_bytes": ([I] * 6 + [U], S),
@@ -144,7 +146,7 @@ def backward(q, k, v, k2, v2, o, lse, dO, w1: int, w2: int, det: bool = False, o
         raise SimplicialAttnError("o must be in the output dtype and dO in the input dtype, contiguous")
     dq = torch.empty((B, N, H, D), dtype=od, device=q.device)
     dk, dv, dk2, dv2 = (torch.empty_like(k, dtype=od) for _ in range(4))
-    wsb = int(L.simplicial_attn_bwd_workspace_bytes(B, H, N, D, w1, w2, flags))
+    wsb = int(L.simplicial_attn_bwd_workspace_bytes_prefixed(B, H, N, D, w1, w2, n_prefix, flags))
     if workspace is None or workspace.numel() < wsb:
         workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=q.device)
     st = L.simplicial_attn_bwd_prefixed(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),

@@ -131,11 +131,16 @@ sa_status simplicial_attn_fwd(const void* q, const void* k, const void* v, const
   return simplicial_attn_fwd_prefixed(q, k, v, k2, v2, o, lse, B, H, N, D, w1, w2, 0, flags, stream);
 }
 
+size_t simplicial_attn_bwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                                    int64_t w2, int64_t n_prefix, uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p) != SA_OK) return 0;
+  return bwd_ws(p, flags);
+}
+
 size_t simplicial_attn_bwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
                                            uint32_t flags) {
-  Problem p;
-  if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
-  return bwd_ws(p, flags);
+  return simplicial_attn_bwd_workspace_bytes_prefixed(B, H, N, D, w1, w2, 0, flags);
 }
 
 sa_status simplicial_attn_bwd_prefixed(const void* q, const void* k, const void* v, const void* k2,

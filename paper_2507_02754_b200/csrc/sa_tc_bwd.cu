@@ -517,6 +517,324 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
   }
 }
 
+// ==========================================================================================
+// bwd_kv: dK, dV (K/V-stationary).  TMEM lanes = key rows j of the CTA's 128-row block.
+// ==========================================================================================
+constexpr int kKVThreads = 384;
+constexpr uint32_t kKST = 0, kKdPT = 128, kKdV = 256, kKdK = 384;
+
+struct BwdKVArgs {
+  Problem p;  // after the swap: w1 = long window (this kernel's keys), w2 = R
+  const __nv_bfloat16 *q, *k2, *v2, *dO;
+  const float *lse, *delta;
+  void *dk, *dv;
+  int out_f32, R, G;
+};
+
+template <int D>
+struct KVSmem {
+  static constexpr int kPanelBytes = 128 * 128;  // 128 rows x 64 fp16
+  static constexpr int kTileBytes = 128 * D * 2;
+  alignas(1024) uint8_t kb[kTileBytes];
+  alignas(1024) uint8_t vb[kTileBytes];
+  alignas(1024) uint8_t as[2][kTileBytes];
+  alignas(1024) uint8_t adp[2][kTileBytes];
+  float2 rinfo[2][128];  // (lse * log2e or +inf for invalid rows, delta)
+  uint64_t kvload, aready[2], afree[2], sfull, pready, done;
+  uint32_t tmem_base;
+};
+
+// 16-byte chunk (row, c8) of a K-major SWIZZLE_128B tile of 128 rows: panel c8/8, chunk c8%8
+// XOR (row%8) -- the layout TMA writes and the UMMA descriptor reads.
+__device__ __forceinline__ uint32_t sw128_off(int row, int c8) {
+  return uint32_t((c8 >> 3) * (128 * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4));
+}
+
+template <int D, bool DET>
+__global__ void __launch_bounds__(kKVThreads, 1)
+    tc_bwd_kv_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdKVArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  static_assert(sizeof(KVSmem<D>) + 1024 <= 232448, "shared memory budget");
+  KVSmem<D>& sm = *reinterpret_cast<KVSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Problem& p = a.p;
+  constexpr int kPanels = D / 64;
+  constexpr uint32_t kPanelBytes = KVSmem<D>::kPanelBytes;
+  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int j0 = blockIdx.x * 128;
+  // queries touching key rows [j0, j0+128): positions [j0, j0+127+w1-1] within [np, np+N)
+  const int qa = max(j0, p.np) - p.np;
+  const int qb = min(j0 + 128 + p.w1 - 1, p.np + p.N) - p.np;
+  const int ntile = qb > qa ? (qb - qa + a.G - 1) / a.G : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(&sm.kvload, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.aready[s], 3);
+      mbar_init(&sm.afree[s], 1);
+    }
+    mbar_init(&sm.sfull, 1);
+    mbar_init(&sm.pready, 8);
+    mbar_init(&sm.done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // ------------------------------ TMA (once) + A-tile formers ------------------------------
+    if (warp == 0 && lane == 0 && ntile > 0) {
+      mbar_expect_tx(&sm.kvload, 2 * KVSmem<D>::kTileBytes);
+      for (int pn = 0; pn < kPanels; ++pn) {
+        tma_load_4d(sm.kb + pn * kPanelBytes, &tmK, &sm.kvload, pn * 64, h, j0, b);
+        tma_load_4d(sm.vb + pn * kPanelBytes, &tmV, &sm.kvload, pn * 64, h, j0, b);
+      }
+    }
+    const int ft = (warp == 0 ? 0 : warp - 1) * 32 + lane;  // 0..95
+    constexpr int kNF = 96;
+    for (int t = 0; t < ntile; ++t) {
+      const int buf = t & 1;
+      mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
+      const int q0 = qa + t * a.G;
+      // row info
+      for (int r = ft; r < 128; r += kNF) {
+        const int g = r / a.R, kk = r % a.R;
+        const int i = q0 + g;
+        const int kpos = p.np + i - a.R + 1 + kk;
+        const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
+        float2 ri = make_float2(INFINITY, 0.f);
+        if (valid) {
+          const int64_t x = (int64_t(b) * p.H + h) * p.N + i;
+          ri = make_float2(a.lse[x] * kLog2e, a.delta[x]);
+        }
+        sm.rinfo[buf][r] = ri;
+      }
+      // A_S = s (q o k2) [det: s (k2 x q)], A_dP = dO o v2  -> swizzled fp16 tiles
+      constexpr int kWS = DET ? 24 : 8;                 // A_S task width (elements)
+      constexpr int kTS = (D + kWS - 1) / kWS;          // A_S tasks per row
+      constexpr int kTD = D / 8;                        // A_dP tasks per row
+      for (int task = ft; task < 128 * (kTS + kTD); task += kNF) {
+        const int r = task / (kTS + kTD), tk = task % (kTS + kTD);
+        const int g = r / a.R, kk = r % a.R;
+        const int i = q0 + g;
+        const int kpos = p.np + i - a.R + 1 + kk;
+        const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
+        if (tk < kTS) {
+          const int e0 = tk * kWS;
+          uint32_t pk[kWS / 2];
+#pragma unroll
+          for (int e = 0; e < kWS / 2; ++e) pk[e] = 0u;
+          if (valid) {
+            const __nv_bfloat16* qr = a.q + p.qoff(b, i, h) + e0;
+            const __nv_bfloat16* kr = a.k2 + p.koff(b, kpos, h) + e0;
+            if (DET) {
+              constexpr int D3 = (D / 3) * 3;
+              float xf[24], yf[24];
+#pragma unroll
+              for (int u = 0; u < kWS / 8; ++u) {
+                float tx[8], ty[8];
+                if (e0 + 8 * u < D) {
+                  load_bf16<8>(qr + 8 * u, tx);
+                  load_bf16<8>(kr + 8 * u, ty);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) tx[e] = ty[e] = 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  xf[8 * u + e] = tx[e];
+                  yf[8 * u + e] = ty[e];
+                }
+              }
+#pragma unroll
+              for (int c3 = 0; c3 < kWS; c3 += 3) {
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+                if (e0 + c3 + 3 <= D3) {  // (k2 x q)
+                  a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+                  a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+                  a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+                }
+                xf[c3] = a0;  // reuse xf as the output vector
+                xf[c3 + 1] = a1;
+                xf[c3 + 2] = a2;
+              }
+#pragma unroll
+              for (int e = 0; e < kWS / 2; ++e) pk[e] = pack_f16x2(p.scale * xf[2 * e], p.scale * xf[2 * e + 1]);
+            } else {
+              float tx[8], ty[8];
+              load_bf16<8>(qr, tx);
+              load_bf16<8>(kr, ty);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                pk[e] = pack_f16x2(p.scale * tx[2 * e] * ty[2 * e], p.scale * tx[2 * e + 1] * ty[2 * e + 1]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kWS / 8; ++u)
+            if (e0 + 8 * u < D)
+              *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r, e0 / 8 + u)) =
+                  make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        } else {
+          const int c8 = tk - kTS;
+          uint32_t pk[4] = {0u, 0u, 0u, 0u};
+          if (valid) {
+            float tx[8], ty[8];
+            load_bf16<8>(a.dO + p.qoff(b, i, h) + 8 * c8, tx);
+            load_bf16<8>(a.v2 + p.koff(b, kpos, h) + 8 * c8, ty);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk[e] = pack_f16x2(tx[2 * e] * ty[2 * e], tx[2 * e + 1] * ty[2 * e + 1]);
+          }
+          *reinterpret_cast<uint4*>(sm.adp[buf] + sw128_off(r, c8)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.aready[buf]);
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer ------------------------------
+    if (lane == 0 && ntile > 0) {
+      const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
+      const uint32_t idesc_s = idesc_f16(128, 128, 0, 0);
+      const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
+      const uint32_t kaddr = smem_u32(sm.kb), vaddr = smem_u32(sm.vb);
+      mbar_wait(&sm.kvload, 0);
+      for (int t = 0; t < ntile; ++t) {
+        const int buf = t & 1;
+        mbar_wait(&sm.aready[buf], (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+          mma_ss(tST, smem_desc_sw128(kaddr + off, 16, 1024), smem_desc_sw128(asa + off, 16, 1024), idesc_s,
+                 kk > 0 ? 1u : 0u);
+          mma_ss(tdPT, smem_desc_sw128(vaddr + off, 16, 1024), smem_desc_sw128(ada + off, 16, 1024), idesc_s,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.sfull);
+        mbar_wait(&sm.pready, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
+          mma_ts(tdV, tST + kk * 8, smem_desc_sw128(ada + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+          mma_ts(tdK, tdPT + kk * 8, smem_desc_sw128(asa + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+        }
+        mma_commit(&sm.afree[buf]);
+      }
+      mma_commit(&sm.done);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------ P^T, dS^T and the dK/dV epilogue ------------------------------
+    const int qd = warp & 3, half = (warp - 4) >> 2;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t tST = tbase + kKST + lane_off, tdPT = tbase + kKdPT + lane_off;
+    const uint32_t tdV = tbase + kKdV + lane_off, tdK = tbase + kKdK + lane_off;
+    const int j = j0 + qd * 32 + lane;     // this thread's key row
+    const int jw0 = j0 + qd * 32;          // warp's first key row
+    const int cb = 64 * half;              // tile columns (rows (i,k)) handled by this half
+    for (int t = 0; t < ntile; ++t) {
+      const int buf = t & 1;
+      const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
+      mbar_wait(&sm.sfull, t & 1);
+      tc_fence_after();
+      uint32_t su[64], du[64];
+      tmem_ld32(tST + cb, *reinterpret_cast<uint32_t(*)[32]>(su));
+      tmem_ld32(tST + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(su + 32));
+      tmem_ld32(tdPT + cb, *reinterpret_cast<uint32_t(*)[32]>(du));
+      tmem_ld32(tdPT + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(du + 32));
+      tmem_ld_wait();
+      // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
+      // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
+      const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
+      int clo = 0, chi = 127;
+      if (!all_in) {
+        const int glo = max(0, j - P0), ghi = min(a.G - 1, j - P0 + p.w1 - 1);
+        clo = glo * a.R - cb;
+        chi = (ghi + 1) * a.R - 1 - cb;
+        if (ghi < glo) { clo = 1; chi = 0; }
+      }
+      uint32_t pp[32], pd[32];
+#pragma unroll
+      for (int t2 = 0; t2 < 32; ++t2) {
+        const float2 r0 = sm.rinfo[buf][cb + 2 * t2], r1 = sm.rinfo[buf][cb + 2 * t2 + 1];
+        float p0 = ex2(fmaf(__uint_as_float(su[2 * t2]), kLog2e, -r0.x));
+        float p1 = ex2(fmaf(__uint_as_float(su[2 * t2 + 1]), kLog2e, -r1.x));
+        if (!all_in) {
+          p0 = (2 * t2 >= clo && 2 * t2 <= chi) ? p0 : 0.f;
+          p1 = (2 * t2 + 1 >= clo && 2 * t2 + 1 <= chi) ? p1 : 0.f;
+        }
+        pp[t2] = pack_f16x2(p0, p1);
+        pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[2 * t2]) - r0.y), p1 * (__uint_as_float(du[2 * t2 + 1]) - r1.y));
+      }
+      tmem_st32(tST + 32 * half, pp);
+      tmem_st32(tdPT + 32 * half, pd);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.pready);
+    }
+    // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns
+    if (ntile > 0) {
+      mbar_wait(&sm.done, 0);
+      tc_fence_after();
+    }
+    if (j < p.NK()) {
+#pragma unroll
+      for (int t2 = 0; t2 < D / 64; ++t2) {
+        const int c0 = half * (D / 2) + 32 * t2;
+        uint32_t uv[32], uk[32];
+        if (ntile > 0) {
+          tmem_ld32(tdV + c0, uv);
+          tmem_ld32(tdK + c0, uk);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) uv[e] = uk[e] = 0u;
+        }
+        const int64_t off = p.koff(b, j, h) + c0;
+        if (a.out_f32) {
+          float4* dv4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dv) + off);
+          float4* dk4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dk) + off);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            dv4[e] = make_float4(__uint_as_float(uv[4 * e]), __uint_as_float(uv[4 * e + 1]),
+                                 __uint_as_float(uv[4 * e + 2]), __uint_as_float(uv[4 * e + 3]));
+            dk4[e] = make_float4(__uint_as_float(uk[4 * e]), __uint_as_float(uk[4 * e + 1]),
+                                 __uint_as_float(uk[4 * e + 2]), __uint_as_float(uk[4 * e + 3]));
+          }
+        } else {
+          uint4* dv4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dv) + off);
+          uint4* dk4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dk) + off);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t w[4], x[4];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+              __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(uv[8 * e + 2 * f]), __uint_as_float(uv[8 * e + 2 * f + 1]));
+              __nv_bfloat162 hk = __floats2bfloat162_rn(__uint_as_float(uk[8 * e + 2 * f]), __uint_as_float(uk[8 * e + 2 * f + 1]));
+              w[f] = *reinterpret_cast<uint32_t*>(&hv);
+              x[f] = *reinterpret_cast<uint32_t*>(&hk);
+            }
+            dv4[e] = make_uint4(w[0], w[1], w[2], w[3]);
+            dk4[e] = make_uint4(x[0], x[1], x[2], x[3]);
+          }
+        }
+      }
+    }
+  }
+
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_free<512>(tbase);
+}
+
 }  // namespace
 
 cudaError_t simt_bwd_dk_only(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
@@ -648,8 +966,44 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
-  // bwd_kv: dk, dv (bring-up: CUDA-core kernel)
-  return simt_bwd_dk_only(p, out_f32, q, k, v, k2, v2, dO, lse, delta, dk, dv, st);
+  // bwd_kv: dk, dv
+  {
+    CUtensorMap tmK, tmV;
+    if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.H, p.D, 128) ||
+        !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.H, p.D, 128))
+      return cudaErrorInvalidValue;
+    BwdKVArgs a;
+    a.p = p;
+    a.q = (const __nv_bfloat16*)q;
+    a.k2 = (const __nv_bfloat16*)k2;
+    a.v2 = (const __nv_bfloat16*)v2;
+    a.dO = (const __nv_bfloat16*)dO;
+    a.lse = lse;
+    a.delta = delta;
+    a.dk = dk;
+    a.dv = dv;
+    a.out_f32 = out_f32 ? 1 : 0;
+    a.R = R;
+    a.G = G;
+    dim3 grid((p.NK() + 127) / 128, p.B * p.H);
+    auto launch = [&](auto kern, size_t smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      KernelScope ks("tc_bwd_kv", st);
+      kern<<<grid, kKVThreads, smem, st>>>(tmK, tmV, a);
+    };
+    if (p.D == 128) {
+      if (p.det)
+        launch(tc_bwd_kv_kernel<128, true>, sizeof(KVSmem<128>) + 1024);
+      else
+        launch(tc_bwd_kv_kernel<128, false>, sizeof(KVSmem<128>) + 1024);
+    } else {
+      if (p.det)
+        launch(tc_bwd_kv_kernel<64, true>, sizeof(KVSmem<64>) + 1024);
+      else
+        launch(tc_bwd_kv_kernel<64, false>, sizeof(KVSmem<64>) + 1024);
+    }
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace sa
