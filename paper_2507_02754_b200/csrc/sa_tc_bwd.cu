@@ -785,12 +785,12 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_wait(&sm.done, 0);
       tc_fence_after();
     }
-    if (j < p.NK()) {
+    {
 #pragma unroll
       for (int t2 = 0; t2 < D / 64; ++t2) {
         const int c0 = half * (D / 2) + 32 * t2;
         uint32_t uv[32], uk[32];
-        if (ntile > 0) {
+        if (ntile > 0) {  // warp-uniform: tcgen05.ld is .sync.aligned, never under a per-lane branch
           tmem_ld32(tdV + c0, uv);
           tmem_ld32(tdK + c0, uk);
           tmem_ld_wait();
@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) uv[e] = uk[e] = 0u;
         }
+        if (j >= p.NK()) continue;
         const int64_t off = p.koff(b, j, h) + c0;
         if (a.out_f32) {
           float4* dv4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dv) + off);
