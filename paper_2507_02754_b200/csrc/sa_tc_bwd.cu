@@ -298,8 +298,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
           tc_fence_after();
           for (int kk = 0; kk < w / 16; ++kk) {
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-            mma_ts(tW, tdP + kk * 8, smem_desc_sw128(kaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
-            mma_ts(tU, tS + kk * 8, smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+            // P / dS of chunk columns [32h, 32h+32) live in TMEM columns [32h, 32h+16) (own region)
+            const uint32_t pc = 32 * (kk >> 1) + 8 * (kk & 1);
+            mma_ts(tW, tdP + pc, smem_desc_sw128(kaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+            mma_ts(tU, tS + pc, smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
           }
           mma_commit(&sm.kvempty[s]);
         }
@@ -405,11 +407,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
             }
           }
           if (nw == 32) {
-            tmem_st16(tS + 16 * half, pp);
-            tmem_st16(tdP + 16 * half, pd);
+            tmem_st16(tS + 32 * half, pp);
+            tmem_st16(tdP + 32 * half, pd);
           } else {
-            tmem_st8(tS + 16 * half, pp);
-            tmem_st8(tdP + 16 * half, pd);
+            tmem_st8(tS + 32 * half, pp);
+            tmem_st8(tdP + 32 * half, pd);
           }
           tmem_st_wait();
         }
@@ -519,16 +521,24 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
 
 // ==========================================================================================
 // bwd_kv: dK, dV (K/V-stationary).  TMEM lanes = key rows j of the CTA's 128-row block.
+// The row tile's columns are processed in two halves (tile rows 0-63 / 64-127) so that the
+// softmax-gradient of one half overlaps the MMAs of the other:
+//   S^T_a, dP^T_a | S^T_b, dP^T_b | (P_a ready) dV,dK += half a | (P_b ready) dV,dK += half b
+// A tiles (A_S = q o k2 [det k2 x q], A_dP = dO o v2, fp16, unscaled: s is folded into the
+// exponent and the dK epilogue) are formed by 3 former warps from an fp16 staging ring filled
+// with cp.async one tile ahead.
 // ==========================================================================================
 constexpr int kKVThreads = 384;
 constexpr uint32_t kKST = 0, kKdPT = 128, kKdV = 256, kKdK = 384;
+constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
+constexpr int kKVGmax = 8;    // staged queries per tile
 
 struct BwdKVArgs {
   Problem p;  // after the swap: w1 = long window (this kernel's keys), w2 = R
-  const __nv_bfloat16 *q, *k2, *v2, *dO;
+  const __half *q, *k2, *v2, *dO;  // fp16 copies
   const float *lse, *delta;
   void *dk, *dv;
-  int out_f32, R, G;
+  int out_f32, R, G, ring;
 };
 
 template <int D>
@@ -539,8 +549,13 @@ struct KVSmem {
   alignas(1024) uint8_t vb[kTileBytes];
   alignas(1024) uint8_t as[2][kTileBytes];
   alignas(1024) uint8_t adp[2][kTileBytes];
+  alignas(16) __half rk2[kKVRing][D];
+  alignas(16) __half rv2[kKVRing][D];
+  alignas(16) __half sq[2][kKVGmax][D];
+  alignas(16) __half sdo[2][kKVGmax][D];
+  float slse[2][kKVGmax], sdl[2][kKVGmax];
   float2 rinfo[2][128];  // (lse * log2e or +inf for invalid rows, delta)
-  uint64_t kvload, aready[2], afree[2], sfull, pready, done;
+  uint64_t kvload, aready[2], afree[2], sfull[2], pready[2], done;
   uint32_t tmem_base;
 };
 
@@ -550,7 +565,12 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int c8) {
   return uint32_t((c8 >> 3) * (128 * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4));
 }
 
-template <int D, bool DET>
+__device__ __forceinline__ uint32_t hmul2_u32(uint32_t x, uint32_t y) {
+  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&x), *reinterpret_cast<__half2*>(&y));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+template <int D, bool DET, bool STAGED>
 __global__ void __launch_bounds__(kKVThreads, 1)
     tc_bwd_kv_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdKVArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -560,6 +580,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   const Problem& p = a.p;
   constexpr int kPanels = D / 64;
   constexpr uint32_t kPanelBytes = KVSmem<D>::kPanelBytes;
+  constexpr int kC8 = D / 8;  // 16-byte chunks per row
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int j0 = blockIdx.x * 128;
   // queries touching key rows [j0, j0+128): positions [j0, j0+127+w1-1] within [np, np+N)
@@ -574,9 +595,9 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.aready[s], 3);
       mbar_init(&sm.afree[s], 1);
+      mbar_init(&sm.sfull[s], 1);
+      mbar_init(&sm.pready[s], 4);
     }
-    mbar_init(&sm.sfull, 1);
-    mbar_init(&sm.pready, 8);
     mbar_init(&sm.done, 1);
     fence_mbar_init();
   }
@@ -597,11 +618,52 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     }
     const int ft = (warp == 0 ? 0 : warp - 1) * 32 + lane;  // 0..95
     constexpr int kNF = 96;
+    // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
+    auto stage = [&](int t) {
+      const int q0 = qa + t * a.G, P0 = p.np + q0;
+      const int klo = t == 0 ? P0 - a.R + 1 : P0, khi = P0 + a.G - 1;
+      const int nk = khi - klo + 1;
+      for (int task = ft; task < nk * kC8 * 2; task += kNF) {
+        const int which = task / (nk * kC8), rem = task % (nk * kC8);
+        const int kp = klo + rem / kC8, c8 = rem % kC8;
+        if (kp < 0 || kp >= p.NK()) continue;
+        const __half* src = (which ? a.v2 : a.k2) + p.koff(b, kp, h) + 8 * c8;
+        __half* dst = (which ? &sm.rv2[0][0] : &sm.rk2[0][0]) + (kp % a.ring) * D + 8 * c8;
+        cp_async16(dst, src);
+      }
+      const int nq = min(a.G, qb - q0);
+      for (int task = ft; task < nq * kC8 * 2; task += kNF) {
+        const int which = task / (nq * kC8), rem = task % (nq * kC8);
+        const int g = rem / kC8, c8 = rem % kC8;
+        const __half* src = (which ? a.dO : a.q) + p.qoff(b, q0 + g, h) + 8 * c8;
+        __half* dst = (which ? &sm.sdo[t & 1][0][0] : &sm.sq[t & 1][0][0]) + g * D + 8 * c8;
+        cp_async16(dst, src);
+      }
+      if (ft < 2 * nq) {
+        const int g = ft % nq;
+        const int64_t x = (int64_t(b) * p.H + h) * p.N + q0 + g;
+        if (ft < nq)
+          cp_async4(&sm.slse[t & 1][g], a.lse + x);
+        else
+          cp_async4(&sm.sdl[t & 1][g], a.delta + x);
+      }
+      cp_async_commit();
+    };
+    if (STAGED && ntile > 0) stage(0);
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
-      mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
       const int q0 = qa + t * a.G;
-      // row info
+      if (STAGED) {
+        if (t + 1 < ntile) {
+          stage(t + 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        named_bar_sync(2, kNF);
+      }
+      mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
+      // row info: (lse * log2e, delta), +inf marks rows outside the problem
       for (int r = ft; r < 128; r += kNF) {
         const int g = r / a.R, kk = r % a.R;
         const int i = q0 + g;
@@ -609,98 +671,110 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
         float2 ri = make_float2(INFINITY, 0.f);
         if (valid) {
-          const int64_t x = (int64_t(b) * p.H + h) * p.N + i;
-          ri = make_float2(a.lse[x] * kLog2e, a.delta[x]);
+          if (STAGED) {
+            ri = make_float2(sm.slse[buf][g] * kLog2e, sm.sdl[buf][g]);
+          } else {
+            const int64_t x = (int64_t(b) * p.H + h) * p.N + i;
+            ri = make_float2(a.lse[x] * kLog2e, a.delta[x]);
+          }
         }
         sm.rinfo[buf][r] = ri;
       }
-      // A_S = s (q o k2) [det: s (k2 x q)], A_dP = dO o v2  -> swizzled fp16 tiles
-      constexpr int kWS = DET ? 24 : 8;                 // A_S task width (elements)
-      constexpr int kTS = (D + kWS - 1) / kWS;          // A_S tasks per row
-      constexpr int kTD = D / 8;                        // A_dP tasks per row
-      for (int task = ft; task < 128 * (kTS + kTD); task += kNF) {
-        const int r = task / (kTS + kTD), tk = task % (kTS + kTD);
+      // A_S = q o k2 [det: k2 x q], A_dP = dO o v2 -> swizzled fp16 tiles
+      constexpr int kWS = DET ? 24 : 8;       // A_S task width (elements)
+      constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
+      constexpr int kTasks = DET ? kTS + kC8 : kC8;
+      for (int task = ft; task < 128 * kTasks; task += kNF) {
+        const int r = task / kTasks, tk = task % kTasks;
         const int g = r / a.R, kk = r % a.R;
         const int i = q0 + g;
         const int kpos = p.np + i - a.R + 1 + kk;
         const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
-        if (tk < kTS) {
-          const int e0 = tk * kWS;
-          uint32_t pk[kWS / 2];
-#pragma unroll
-          for (int e = 0; e < kWS / 2; ++e) pk[e] = 0u;
+        const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
+        const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
+        const __half* k2row = STAGED ? &sm.rk2[kpos % a.ring][0] : a.k2 + p.koff(b, kpos, h);
+        const __half* v2row = STAGED ? &sm.rv2[kpos % a.ring][0] : a.v2 + p.koff(b, kpos, h);
+        if (!DET) {
+          uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
           if (valid) {
-            const __nv_bfloat16* qr = a.q + p.qoff(b, i, h) + e0;
-            const __nv_bfloat16* kr = a.k2 + p.koff(b, kpos, h) + e0;
-            if (DET) {
-              constexpr int D3 = (D / 3) * 3;
-              float xf[24], yf[24];
+            const uint4 x = *reinterpret_cast<const uint4*>(qrow + 8 * tk);
+            const uint4 y = *reinterpret_cast<const uint4*>(k2row + 8 * tk);
+            const uint4 u = *reinterpret_cast<const uint4*>(dorow + 8 * tk);
+            const uint4 w = *reinterpret_cast<const uint4*>(v2row + 8 * tk);
+            oa = make_uint4(hmul2_u32(x.x, y.x), hmul2_u32(x.y, y.y), hmul2_u32(x.z, y.z), hmul2_u32(x.w, y.w));
+            od = make_uint4(hmul2_u32(u.x, w.x), hmul2_u32(u.y, w.y), hmul2_u32(u.z, w.z), hmul2_u32(u.w, w.w));
+          }
+          *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r, tk)) = oa;
+          *reinterpret_cast<uint4*>(sm.adp[buf] + sw128_off(r, tk)) = od;
+        } else if (tk < kTS) {
+          const int e0 = tk * kWS;
+          uint32_t pk[12];
 #pragma unroll
-              for (int u = 0; u < kWS / 8; ++u) {
-                float tx[8], ty[8];
-                if (e0 + 8 * u < D) {
-                  load_bf16<8>(qr + 8 * u, tx);
-                  load_bf16<8>(kr + 8 * u, ty);
-                } else {
+          for (int e = 0; e < 12; ++e) pk[e] = 0u;
+          if (valid) {
+            constexpr int D3 = (D / 3) * 3;
+            float xf[24], yf[24];
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) tx[e] = ty[e] = 0.f;
+            for (int u = 0; u < 3; ++u) {
+              if (e0 + 8 * u < D) {
+                const uint4 x = *reinterpret_cast<const uint4*>(qrow + e0 + 8 * u);
+                const uint4 y = *reinterpret_cast<const uint4*>(k2row + e0 + 8 * u);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 fx = __half22float2(*reinterpret_cast<const __half2*>(&xs[e]));
+                  const float2 fy = __half22float2(*reinterpret_cast<const __half2*>(&ys[e]));
+                  xf[8 * u + 2 * e] = fx.x;
+                  xf[8 * u + 2 * e + 1] = fx.y;
+                  yf[8 * u + 2 * e] = fy.x;
+                  yf[8 * u + 2 * e + 1] = fy.y;
                 }
+              } else {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  xf[8 * u + e] = tx[e];
-                  yf[8 * u + e] = ty[e];
-                }
+                for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
               }
-#pragma unroll
-              for (int c3 = 0; c3 < kWS; c3 += 3) {
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-                if (e0 + c3 + 3 <= D3) {  // (k2 x q)
-                  a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
-                  a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
-                  a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
-                }
-                xf[c3] = a0;  // reuse xf as the output vector
-                xf[c3 + 1] = a1;
-                xf[c3 + 2] = a2;
-              }
-#pragma unroll
-              for (int e = 0; e < kWS / 2; ++e) pk[e] = pack_f16x2(p.scale * xf[2 * e], p.scale * xf[2 * e + 1]);
-            } else {
-              float tx[8], ty[8];
-              load_bf16<8>(qr, tx);
-              load_bf16<8>(kr, ty);
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                pk[e] = pack_f16x2(p.scale * tx[2 * e] * ty[2 * e], p.scale * tx[2 * e + 1] * ty[2 * e + 1]);
             }
+#pragma unroll
+            for (int c3 = 0; c3 < 24; c3 += 3) {
+              float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+              if (e0 + c3 + 3 <= D3) {  // (k2 x q)
+                a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+                a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+                a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+              }
+              xf[c3] = a0;
+              xf[c3 + 1] = a1;
+              xf[c3 + 2] = a2;
+            }
+#pragma unroll
+            for (int e = 0; e < 12; ++e) pk[e] = pack_f16x2(xf[2 * e], xf[2 * e + 1]);
           }
 #pragma unroll
-          for (int u = 0; u < kWS / 8; ++u)
+          for (int u = 0; u < 3; ++u)
             if (e0 + 8 * u < D)
               *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r, e0 / 8 + u)) =
                   make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         } else {
           const int c8 = tk - kTS;
-          uint32_t pk[4] = {0u, 0u, 0u, 0u};
+          uint4 od = make_uint4(0u, 0u, 0u, 0u);
           if (valid) {
-            float tx[8], ty[8];
-            load_bf16<8>(a.dO + p.qoff(b, i, h) + 8 * c8, tx);
-            load_bf16<8>(a.v2 + p.koff(b, kpos, h) + 8 * c8, ty);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) pk[e] = pack_f16x2(tx[2 * e] * ty[2 * e], tx[2 * e + 1] * ty[2 * e + 1]);
+            const uint4 u = *reinterpret_cast<const uint4*>(dorow + 8 * c8);
+            const uint4 w = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
+            od = make_uint4(hmul2_u32(u.x, w.x), hmul2_u32(u.y, w.y), hmul2_u32(u.z, w.z), hmul2_u32(u.w, w.w));
           }
-          *reinterpret_cast<uint4*>(sm.adp[buf] + sw128_off(r, c8)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(sm.adp[buf] + sw128_off(r, c8)) = od;
         }
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.aready[buf]);
+      if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
     if (lane == 0 && ntile > 0) {
       const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
-      const uint32_t idesc_s = idesc_f16(128, 128, 0, 0);
+      const uint32_t idesc_s = idesc_f16(128, 64, 0, 0);
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
       const uint32_t kaddr = smem_u32(sm.kb), vaddr = smem_u32(sm.vb);
       mbar_wait(&sm.kvload, 0);
@@ -710,21 +784,29 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         tc_fence_after();
         const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
-          mma_ss(tST, smem_desc_sw128(kaddr + off, 16, 1024), smem_desc_sw128(asa + off, 16, 1024), idesc_s,
-                 kk > 0 ? 1u : 0u);
-          mma_ss(tdPT, smem_desc_sw128(vaddr + off, 16, 1024), smem_desc_sw128(ada + off, 16, 1024), idesc_s,
-                 kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&sm.sfull);
-        mbar_wait(&sm.pready, t & 1);
-        tc_fence_after();
+        for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tdV, tST + kk * 8, smem_desc_sw128(ada + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
-          mma_ts(tdK, tdPT + kk * 8, smem_desc_sw128(asa + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+            const uint32_t boff = off + hh * 64 * 128;
+            mma_ss(tST + 64 * hh, smem_desc_sw128(kaddr + off, 16, 1024), smem_desc_sw128(asa + boff, 16, 1024),
+                   idesc_s, kk > 0 ? 1u : 0u);
+            mma_ss(tdPT + 64 * hh, smem_desc_sw128(vaddr + off, 16, 1024), smem_desc_sw128(ada + boff, 16, 1024),
+                   idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.sfull[hh]);
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          mbar_wait(&sm.pready[hh], t & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (t > 0 || hh > 0 || kk > 0) ? 1u : 0u;
+            const uint32_t roff = (64 * hh + 16 * kk) * 128;
+            mma_ts(tdV, tST + 64 * hh + 8 * kk, smem_desc_sw128(ada + roff, kPanelBytes, 1024), idesc_acc, acc);
+            mma_ts(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
+          }
         }
         mma_commit(&sm.afree[buf]);
       }
@@ -739,10 +821,11 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     const int j = j0 + qd * 32 + lane;     // this thread's key row
     const int jw0 = j0 + qd * 32;          // warp's first key row
     const int cb = 64 * half;              // tile columns (rows (i,k)) handled by this half
+    const float sl2 = p.scale * kLog2e;
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
       const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
-      mbar_wait(&sm.sfull, t & 1);
+      mbar_wait(&sm.sfull[half], t & 1);
       tc_fence_after();
       uint32_t su[64], du[64];
       tmem_ld32(tST + cb, *reinterpret_cast<uint32_t(*)[32]>(su));
@@ -758,14 +841,17 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int glo = max(0, j - P0), ghi = min(a.G - 1, j - P0 + p.w1 - 1);
         clo = glo * a.R - cb;
         chi = (ghi + 1) * a.R - 1 - cb;
-        if (ghi < glo) { clo = 1; chi = 0; }
+        if (ghi < glo) {
+          clo = 1;
+          chi = 0;
+        }
       }
       uint32_t pp[32], pd[32];
 #pragma unroll
       for (int t2 = 0; t2 < 32; ++t2) {
         const float2 r0 = sm.rinfo[buf][cb + 2 * t2], r1 = sm.rinfo[buf][cb + 2 * t2 + 1];
-        float p0 = ex2(fmaf(__uint_as_float(su[2 * t2]), kLog2e, -r0.x));
-        float p1 = ex2(fmaf(__uint_as_float(su[2 * t2 + 1]), kLog2e, -r1.x));
+        float p0 = ex2(fmaf(__uint_as_float(su[2 * t2]), sl2, -r0.x));
+        float p1 = ex2(fmaf(__uint_as_float(su[2 * t2 + 1]), sl2, -r1.x));
         if (!all_in) {
           p0 = (2 * t2 >= clo && 2 * t2 <= chi) ? p0 : 0.f;
           p1 = (2 * t2 + 1 >= clo && 2 * t2 + 1 <= chi) ? p1 : 0.f;
@@ -773,59 +859,61 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         pp[t2] = pack_f16x2(p0, p1);
         pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[2 * t2]) - r0.y), p1 * (__uint_as_float(du[2 * t2 + 1]) - r1.y));
       }
-      tmem_st32(tST + 32 * half, pp);
-      tmem_st32(tdPT + 32 * half, pd);
+      // P^T / dS^T of this half go to the first 32 columns of the half's own S^T / dP^T region
+      tmem_st32(tST + cb, pp);
+      tmem_st32(tdPT + cb, pd);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.pready);
+      if (lane == 0) mbar_arrive(&sm.pready[half]);
     }
-    // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns
+    // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns; dK carries the scale s
     if (ntile > 0) {
       mbar_wait(&sm.done, 0);
       tc_fence_after();
     }
-    {
+    const float ks = p.scale;
 #pragma unroll
-      for (int t2 = 0; t2 < D / 64; ++t2) {
-        const int c0 = half * (D / 2) + 32 * t2;
-        uint32_t uv[32], uk[32];
-        if (ntile > 0) {  // warp-uniform: tcgen05.ld is .sync.aligned, never under a per-lane branch
-          tmem_ld32(tdV + c0, uv);
-          tmem_ld32(tdK + c0, uk);
-          tmem_ld_wait();
-        } else {
+    for (int t2 = 0; t2 < D / 64; ++t2) {
+      const int c0 = half * (D / 2) + 32 * t2;
+      uint32_t uv[32], uk[32];
+      if (ntile > 0) {  // warp-uniform: tcgen05.ld is .sync.aligned, never under a per-lane branch
+        tmem_ld32(tdV + c0, uv);
+        tmem_ld32(tdK + c0, uk);
+        tmem_ld_wait();
+      } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) uv[e] = uk[e] = 0u;
+        for (int e = 0; e < 32; ++e) uv[e] = uk[e] = 0u;
+      }
+      if (j >= p.NK()) continue;
+      const int64_t off = p.koff(b, j, h) + c0;
+      if (a.out_f32) {
+        float4* dv4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dv) + off);
+        float4* dk4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dk) + off);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          dv4[e] = make_float4(__uint_as_float(uv[4 * e]), __uint_as_float(uv[4 * e + 1]),
+                               __uint_as_float(uv[4 * e + 2]), __uint_as_float(uv[4 * e + 3]));
+          dk4[e] = make_float4(ks * __uint_as_float(uk[4 * e]), ks * __uint_as_float(uk[4 * e + 1]),
+                               ks * __uint_as_float(uk[4 * e + 2]), ks * __uint_as_float(uk[4 * e + 3]));
         }
-        if (j >= p.NK()) continue;
-        const int64_t off = p.koff(b, j, h) + c0;
-        if (a.out_f32) {
-          float4* dv4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dv) + off);
-          float4* dk4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dk) + off);
+      } else {
+        uint4* dv4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dv) + off);
+        uint4* dk4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dk) + off);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            dv4[e] = make_float4(__uint_as_float(uv[4 * e]), __uint_as_float(uv[4 * e + 1]),
-                                 __uint_as_float(uv[4 * e + 2]), __uint_as_float(uv[4 * e + 3]));
-            dk4[e] = make_float4(__uint_as_float(uk[4 * e]), __uint_as_float(uk[4 * e + 1]),
-                                 __uint_as_float(uk[4 * e + 2]), __uint_as_float(uk[4 * e + 3]));
+        for (int e = 0; e < 4; ++e) {
+          uint32_t w[4], x[4];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            __nv_bfloat162 hv =
+                __floats2bfloat162_rn(__uint_as_float(uv[8 * e + 2 * f]), __uint_as_float(uv[8 * e + 2 * f + 1]));
+            __nv_bfloat162 hk = __floats2bfloat162_rn(ks * __uint_as_float(uk[8 * e + 2 * f]),
+                                                      ks * __uint_as_float(uk[8 * e + 2 * f + 1]));
+            w[f] = *reinterpret_cast<uint32_t*>(&hv);
+            x[f] = *reinterpret_cast<uint32_t*>(&hk);
           }
-        } else {
-          uint4* dv4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dv) + off);
-          uint4* dk4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.dk) + off);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint32_t w[4], x[4];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              __nv_bfloat162 hv = __floats2bfloat162_rn(__uint_as_float(uv[8 * e + 2 * f]), __uint_as_float(uv[8 * e + 2 * f + 1]));
-              __nv_bfloat162 hk = __floats2bfloat162_rn(__uint_as_float(uk[8 * e + 2 * f]), __uint_as_float(uk[8 * e + 2 * f + 1]));
-              w[f] = *reinterpret_cast<uint32_t*>(&hv);
-              x[f] = *reinterpret_cast<uint32_t*>(&hk);
-            }
-            dv4[e] = make_uint4(w[0], w[1], w[2], w[3]);
-            dk4[e] = make_uint4(x[0], x[1], x[2], x[3]);
-          }
+          dv4[e] = make_uint4(w[0], w[1], w[2], w[3]);
+          dk4[e] = make_uint4(x[0], x[1], x[2], x[3]);
         }
       }
     }
@@ -873,8 +961,8 @@ size_t tc_bwd_workspace_bytes(const Problem& p0) {
   const int R = p.w2, G = 128 / R;
   int pc, items;
   const int grid = q_grid(p, R, G, &pc, &items);
-  const size_t n = size_t(p.B) * p.NK() * p.H * p.D;
-  return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 2 * a256(n * 2) +
+  const size_t n = size_t(p.B) * p.NK() * p.H * p.D, nq = size_t(p.B) * p.N * p.H * p.D;
+  return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 4 * a256(n * 2) + 2 * a256(nq * 2) +
          a256(sizeof(float) * size_t(grid) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
 }
 
@@ -900,6 +988,15 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   w += a256(n * 2);
   char* vf = w;
   w += a256(n * 2);
+  const size_t nq = size_t(p.B) * p.N * p.H * p.D;
+  char* k2f = w;
+  w += a256(n * 2);
+  char* v2f = w;
+  w += a256(n * 2);
+  char* qf = w;
+  w += a256(nq * 2);
+  char* dof = w;
+  w += a256(nq * 2);
   float* band = (float*)w;
 
   // delta
@@ -913,6 +1010,8 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
                                                                              (const __nv_bfloat16*)o, delta);
   }
   cudaError_t e = convert_pair_f16(k, kf, v, vf, int64_t(n), num_sms(), st);
+  if (e == cudaSuccess) e = convert_pair_f16(k2, k2f, v2, v2f, int64_t(n), num_sms(), st);
+  if (e == cudaSuccess) e = convert_pair_f16(q, qf, dO, dof, int64_t(nq), num_sms(), st);
   if (e != cudaSuccess) return e;
 
   // bwd_q: dq, dk2, dv2
@@ -975,10 +1074,10 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
       return cudaErrorInvalidValue;
     BwdKVArgs a;
     a.p = p;
-    a.q = (const __nv_bfloat16*)q;
-    a.k2 = (const __nv_bfloat16*)k2;
-    a.v2 = (const __nv_bfloat16*)v2;
-    a.dO = (const __nv_bfloat16*)dO;
+    a.q = (const __half*)qf;
+    a.k2 = (const __half*)k2f;
+    a.v2 = (const __half*)v2f;
+    a.dO = (const __half*)dof;
     a.lse = lse;
     a.delta = delta;
     a.dk = dk;
@@ -986,22 +1085,25 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
     a.G = G;
+    a.ring = R + 2 * G;
+    const bool staged = G <= kKVGmax && a.ring <= kKVRing;
     dim3 grid((p.NK() + 127) / 128, p.B * p.H);
     auto launch = [&](auto kern, size_t smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       KernelScope ks("tc_bwd_kv", st);
       kern<<<grid, kKVThreads, smem, st>>>(tmK, tmV, a);
     };
+    const size_t s128 = sizeof(KVSmem<128>) + 1024, s64 = sizeof(KVSmem<64>) + 1024;
     if (p.D == 128) {
       if (p.det)
-        launch(tc_bwd_kv_kernel<128, true>, sizeof(KVSmem<128>) + 1024);
+        staged ? launch(tc_bwd_kv_kernel<128, true, true>, s128) : launch(tc_bwd_kv_kernel<128, true, false>, s128);
       else
-        launch(tc_bwd_kv_kernel<128, false>, sizeof(KVSmem<128>) + 1024);
+        staged ? launch(tc_bwd_kv_kernel<128, false, true>, s128) : launch(tc_bwd_kv_kernel<128, false, false>, s128);
     } else {
       if (p.det)
-        launch(tc_bwd_kv_kernel<64, true>, sizeof(KVSmem<64>) + 1024);
+        staged ? launch(tc_bwd_kv_kernel<64, true, true>, s64) : launch(tc_bwd_kv_kernel<64, true, false>, s64);
       else
-        launch(tc_bwd_kv_kernel<64, false>, sizeof(KVSmem<64>) + 1024);
+        staged ? launch(tc_bwd_kv_kernel<64, false, true>, s64) : launch(tc_bwd_kv_kernel<64, false, false>, s64);
     }
   }
   return cudaGetLastError();
