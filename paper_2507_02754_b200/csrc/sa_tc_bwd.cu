@@ -71,7 +71,7 @@ struct BwdQArgs {
   const float *lse, *delta;
   void *dq, *dk2, *dv2;
   float* band;  // [grid][2 start/end][2 k2/v2][R-1][D]
-  int out_f32, R, G, ngroups, items, per_cta, ring;
+  int out_f32, R, lR, G, ngroups, items, per_cta, ring;
 };
 
 template <int D>
@@ -196,6 +196,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
   // dk2 / dv2: key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g)
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
+  const int sbase = (P0 - a.R + 1 + a.ring) % a.ring;
   for (int idx = tid256; idx < nsl * PW; idx += 256) {
     const int sl = idx / PW, d = idx % PW;
     const int kp = P0 - a.R + 1 + sl;
@@ -207,7 +208,8 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
       xk += sm.ek[row][d];
       xv += sm.ev[row][d];
     }
-    const int slot = kp % a.ring;
+    int slot = sbase + sl;  // (P0 - R + 1 + sl) mod ring
+    if (slot >= a.ring) slot -= a.ring;
     sm.acc_k2[slot][c0 + d] += xk;
     sm.acc_v2[slot][c0 + d] += xv;
   }
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
   extern __shared__ uint8_t smem_raw[];
   static_assert(sizeof(QSmem<D>) + 1024 <= 232448, "shared memory budget");
-  QSmem<D>& sm = *reinterpret_cast<QSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  QSmem<D>& sm = *reinterpret_cast<QSmem<D>*>(smem_raw + align1024_pad(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kPanels = D / 64;
   constexpr uint32_t kPanelBytes = QSmem<D>::kPanelBytes;
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         PS = P0;
         flush_lo = P0 - a.R + 1;
       }
-      const int g = r / a.R, kk = r % a.R;
+      const int g = r >> a.lR, kk = r & (a.R - 1);
       const bool row_in = r < a.G * a.R && g < it.nq;
       const int pos = P0 + g;
       const int kpos = pos - a.R + 1 + kk;
@@ -440,10 +442,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool end_open = last_in_sub && PE < p.np + p.N;
       const bool start_open = PS > p.np;
       const int nrows = flush_hi - flush_lo + 1;
+      const int fbase = (flush_lo + a.ring) % a.ring;
       for (int idx = tid256; idx < nrows * D; idx += 256) {
         const int kp = flush_lo + idx / D, d = idx % D;
         if (kp < 0 || kp >= p.NK()) continue;
-        const int slot = kp % a.ring;
+        int slot = fbase + idx / D;
+        if (slot >= a.ring) slot -= a.ring;
         const float vk = sm.acc_k2[slot][d], vv = sm.acc_v2[slot][d];
         sm.acc_k2[slot][d] = 0.f;
         sm.acc_v2[slot][d] = 0.f;
@@ -538,7 +542,7 @@ struct BwdKVArgs {
   const __half *q, *k2, *v2, *dO;  // fp16 copies
   const float *lse, *delta;
   void *dk, *dv;
-  int out_f32, R, G, ring;
+  int out_f32, R, lR, G, ring;
 };
 
 template <int D>
@@ -575,7 +579,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     tc_bwd_kv_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdKVArgs a) {
   extern __shared__ uint8_t smem_raw[];
   static_assert(sizeof(KVSmem<D>) + 1024 <= 232448, "shared memory budget");
-  KVSmem<D>& sm = *reinterpret_cast<KVSmem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  KVSmem<D>& sm = *reinterpret_cast<KVSmem<D>*>(smem_raw + align1024_pad(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Problem& p = a.p;
   constexpr int kPanels = D / 64;
@@ -619,28 +623,39 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     const int ft = (warp == 0 ? 0 : warp - 1) * 32 + lane;  // 0..95
     constexpr int kNF = 96;
     // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
+    auto ring_mod = [&](int kp) {  // kp mod ring for kp >= -ring (one division per call site)
+      return (kp + a.ring) % a.ring;
+    };
     auto stage = [&](int t) {
       const int q0 = qa + t * a.G, P0 = p.np + q0;
       const int klo = t == 0 ? P0 - a.R + 1 : P0, khi = P0 + a.G - 1;
       const int nk = khi - klo + 1;
-      for (int task = ft; task < nk * kC8 * 2; task += kNF) {
-        const int which = task / (nk * kC8), rem = task % (nk * kC8);
-        const int kp = klo + rem / kC8, c8 = rem % kC8;
-        if (kp < 0 || kp >= p.NK()) continue;
-        const __half* src = (which ? a.v2 : a.k2) + p.koff(b, kp, h) + 8 * c8;
-        __half* dst = (which ? &sm.rv2[0][0] : &sm.rk2[0][0]) + (kp % a.ring) * D + 8 * c8;
-        cp_async16(dst, src);
+      const int slo = ring_mod(klo);
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        for (int task = ft; task < nk * kC8; task += kNF) {
+          const int off = task / kC8, c8 = task % kC8;  // kC8 is a compile-time power of two
+          const int kp = klo + off;
+          if (kp < 0 || kp >= p.NK()) continue;
+          int slot = slo + off;
+          if (slot >= a.ring) slot -= a.ring;
+          const __half* src = (which ? a.v2 : a.k2) + p.koff(b, kp, h) + 8 * c8;
+          __half* dst = (which ? &sm.rv2[0][0] : &sm.rk2[0][0]) + slot * D + 8 * c8;
+          cp_async16(dst, src);
+        }
       }
       const int nq = min(a.G, qb - q0);
-      for (int task = ft; task < nq * kC8 * 2; task += kNF) {
-        const int which = task / (nq * kC8), rem = task % (nq * kC8);
-        const int g = rem / kC8, c8 = rem % kC8;
-        const __half* src = (which ? a.dO : a.q) + p.qoff(b, q0 + g, h) + 8 * c8;
-        __half* dst = (which ? &sm.sdo[t & 1][0][0] : &sm.sq[t & 1][0][0]) + g * D + 8 * c8;
-        cp_async16(dst, src);
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        for (int task = ft; task < nq * kC8; task += kNF) {
+          const int g = task / kC8, c8 = task % kC8;
+          const __half* src = (which ? a.dO : a.q) + p.qoff(b, q0 + g, h) + 8 * c8;
+          __half* dst = (which ? &sm.sdo[t & 1][0][0] : &sm.sq[t & 1][0][0]) + g * D + 8 * c8;
+          cp_async16(dst, src);
+        }
       }
       if (ft < 2 * nq) {
-        const int g = ft % nq;
+        const int g = ft < nq ? ft : ft - nq;
         const int64_t x = (int64_t(b) * p.H + h) * p.N + q0 + g;
         if (ft < nq)
           cp_async4(&sm.slse[t & 1][g], a.lse + x);
@@ -664,10 +679,12 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
       // row info: (lse * log2e, delta), +inf marks rows outside the problem
+      const int kbase = p.np + q0 - a.R + 1;  // key row of tile row 0
+      const int sbase = STAGED ? ring_mod(kbase) : 0;
       for (int r = ft; r < 128; r += kNF) {
-        const int g = r / a.R, kk = r % a.R;
+        const int g = r >> a.lR, kk = r & (a.R - 1);
         const int i = q0 + g;
-        const int kpos = p.np + i - a.R + 1 + kk;
+        const int kpos = kbase + g + kk;
         const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
         float2 ri = make_float2(INFINITY, 0.f);
         if (valid) {
@@ -686,14 +703,16 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
       for (int task = ft; task < 128 * kTasks; task += kNF) {
         const int r = task / kTasks, tk = task % kTasks;
-        const int g = r / a.R, kk = r % a.R;
+        const int g = r >> a.lR, kk = r & (a.R - 1);
         const int i = q0 + g;
-        const int kpos = p.np + i - a.R + 1 + kk;
+        const int kpos = kbase + g + kk;
         const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
+        int slot = sbase + g + kk;
+        if (slot >= a.ring) slot -= a.ring;
         const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
         const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
-        const __half* k2row = STAGED ? &sm.rk2[kpos % a.ring][0] : a.k2 + p.koff(b, kpos, h);
-        const __half* v2row = STAGED ? &sm.rv2[kpos % a.ring][0] : a.v2 + p.koff(b, kpos, h);
+        const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
+        const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
         if (!DET) {
           uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
           if (valid) {
@@ -935,7 +954,7 @@ static bool swapped(const Problem& p) { return p.w1 < p.w2; }
 bool tc_bwd_supported(const Problem& p) {
   const int R = swapped(p) ? p.w1 : p.w2;
   if (!(p.D == 64 || p.D == 128)) return false;
-  if (R < 2 || R > kMaxR) return false;
+  if (R < 2 || R > kMaxR || (R & (R - 1))) return false;  // power-of-two rows per query
   const int G = 128 / R;
   return R + G <= kRingMax;
 }
@@ -1034,6 +1053,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.band = band;
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
+    a.lR = __builtin_ctz(unsigned(R));
     a.G = G;
     a.ngroups = (p.N + G - 1) / G;
     a.ring = R + G;
@@ -1084,6 +1104,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.dv = dv;
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
+    a.lR = __builtin_ctz(unsigned(R));
     a.G = G;
     a.ring = R + 2 * G;
     const bool staged = G <= kKVGmax && a.ring <= kKVRing;

@@ -18,6 +18,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Bytes to add to the dynamic shared-memory base to reach 1024-byte alignment (SWIZZLE_128B atoms).
+// Computed from the shared-window address so that `base + pad` stays a shared-space pointer and
+// the compiler emits LDS/STS (a uintptr_t round trip would degrade every access to generic LD/ST).
+__device__ __forceinline__ uint32_t align1024_pad(const void* base) {
+  return (1024u - (smem_u32(base) & 1023u)) & 1023u;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   static_assert(sizeof(Smem<D>) + 1024 <= 232448, "shared memory budget");
-  Smem<D>& sm = *reinterpret_cast<Smem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw + align1024_pad(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kPanels = D / 64 > 0 ? D / 64 : 1;
   constexpr uint32_t kPanelBytes = kChunk * 128;
