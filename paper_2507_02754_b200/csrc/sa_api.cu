@@ -11,6 +11,11 @@
 
 namespace sa {
 
+#ifdef SA_TRACE
+__device__ unsigned long long g_trace[8192];
+__device__ unsigned int g_trace_n;
+#endif
+
 static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(uint64_t(n), std::memory_order_relaxed); }
 
@@ -301,5 +306,19 @@ const char* simplicial_attn_status_string(sa_status s) {
 }
 
 const char* simplicial_attn_version(void) { return "libsimplicial sm_100a " __DATE__ " " __TIME__; }
+
+#ifdef SA_TRACE
+// Trace builds only: copy the (tag, clock) pairs recorded since the last call and reset.
+int simplicial_attn_debug_trace(unsigned long long* host, int max_pairs) {
+  cudaDeviceSynchronize();
+  unsigned int n = 0;
+  cudaMemcpyFromSymbol(&n, sa::g_trace_n, sizeof(n));
+  n = n / 2 < unsigned(max_pairs) ? n / 2 : unsigned(max_pairs);
+  cudaMemcpyFromSymbol(host, sa::g_trace, sizeof(unsigned long long) * 2 * n);
+  unsigned int z = 0;
+  cudaMemcpyToSymbol(sa::g_trace_n, &z, sizeof(z));
+  return int(n);
+}
+#endif
 
 }  // extern "C"

@@ -55,3 +55,26 @@ struct KernelScope {
 };
 
 }  // namespace sa
+
+// ---- optional phase tracing (tools/trace_build.py builds a separate library with -DSA_TRACE) ----
+#ifdef SA_TRACE
+namespace sa {
+extern __device__ unsigned long long g_trace[8192];
+extern __device__ unsigned int g_trace_n;
+}
+// record (tag, clock) from the calling thread of CTA 0 when `cond` holds
+#define SA_TRACE_POINT(cond, tag)                                                                    \
+  do {                                                                                              \
+    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0) {                                             \
+      unsigned int _n = atomicAdd(&::sa::g_trace_n, 2u);                                            \
+      if (_n + 1 < 8192) {                                                                          \
+        ::sa::g_trace[_n] = (unsigned long long)(tag);                                              \
+        ::sa::g_trace[_n + 1] = (unsigned long long)clock64();                                      \
+      }                                                                                             \
+    }                                                                                               \
+  } while (0)
+#else
+#define SA_TRACE_POINT(cond, tag) \
+  do {                            \
+  } while (0)
+#endif

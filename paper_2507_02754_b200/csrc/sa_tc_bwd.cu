@@ -279,8 +279,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
       uint32_t kc = 0, gc = 0;
       for (int item = it_begin; item < it_end; ++item) {
         QItem it = q_item(a, item);
+        const bool tr = item - it_begin < 3;
         mbar_wait(&sm.aready, gc & 1);
         tc_fence_after();
+        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 10 << 8);
         for (int c = 0; c < it.nch; ++c) {
           const int s = (kc + c) % kQStages;
           const uint32_t ph = ((kc + c) / kQStages) & 1;
@@ -296,8 +298,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
             mma_ts(tdP, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
           }
           mma_commit(&sm.sfull);
+          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 11 << 8 | c);
           mbar_wait(&sm.pready, (kc + c) & 1);
           tc_fence_after();
+          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 12 << 8 | c);
           for (int kk = 0; kk < w / 16; ++kk) {
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
             // P / dS of chunk columns [32h, 32h+32) live in TMEM columns [32h, 32h+16) (own region)
@@ -326,6 +330,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
     int PS = 0, flush_lo = 0;
     for (int item = it_begin; item < it_end; ++item) {
       QItem it = q_item(a, item);
+      const bool tr = threadIdx.x == 128 && item - it_begin < 3;
+      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 1 << 8);
       const bool first_in_sub = item == it_begin || it.grp == 0;
       const bool last_in_sub = item == it_end - 1 || it.grp == a.ngroups - 1;
       const int P0 = p.np + it.i0;
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.aready);
+        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 2 << 8);
       }
       // ---- chunks: P = exp(S - lse), dS = P (dP - delta) ----
       const int jlo = max(0, pos - p.w1 + 1);
@@ -371,6 +378,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const int nw = max(0, min(32, w - cb));
         mbar_wait(&sm.sfull, (kc + c) & 1);
         tc_fence_after();
+        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 3 << 8 | c);
         if (nw > 0) {
           uint32_t su[32], du[32];
           if (nw == 32) {
@@ -420,10 +428,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pready);
+        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 4 << 8 | c);
       }
       // ---- epilogue ----
       mbar_wait(&sm.udone, gc & 1);
       tc_fence_after();
+      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 5 << 8);
       if (DET) {
 #pragma unroll 1
         for (int c0 = 0; c0 + 24 <= D; c0 += 24)
@@ -436,6 +446,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           q_epilogue_pass<D, 16, DET>(sm, a, it, c0, half, r, valid, g, kpos, tW, tU, tid256);
       }
       tc_fence_before();
+      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 6 << 8);
       // ---- flush ring rows that no later tile of this sub-range touches ----
       const int PE = P0 + it.nq;
       const int flush_hi = last_in_sub ? PE - 1 : P0 + a.G - a.R;  // inclusive
@@ -474,6 +485,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       }
       flush_lo = flush_hi + 1;
       named_bar_sync(1, 256);
+      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 7 << 8);
       kc += it.nch;
       ++gc;
     }
