@@ -38,6 +38,11 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMaxR = 64;  // bwd_q: rows per query (folded window w2) supported by the ring
 constexpr int kRingMax = 66;
 
+__device__ __forceinline__ uint32_t hmul2_u32(uint32_t x, uint32_t y) {
+  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&x), *reinterpret_cast<__half2*>(&y));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
 // ------------------------------------------------------------------------------------------
 // delta_i = <dO_i, o_i>, one warp per query row
 // ------------------------------------------------------------------------------------------
@@ -60,31 +65,34 @@ __global__ void __launch_bounds__(256) delta_kernel(Problem p, const __nv_bfloat
 // bwd_q: dQ, dK2, dV2
 // ==========================================================================================
 constexpr int kQThreads = 384;
-constexpr int kQStages = 3;
 constexpr int kQChunk = 64;
 // TMEM columns
 constexpr uint32_t kQW = 0, kQU = 128, kQS = 256, kQdP = 320, kQAS = 384, kQAdP = 448;
+constexpr int kQStageRows = 80;  // staged rows per tile: q, dO (G each), k2, v2 (R+G-1 each)
 
 struct BwdQArgs {
   Problem p;  // after the swap: w2 = R rows per query
-  const __nv_bfloat16 *q, *k2, *v2, *dO;
+  const __half *q, *k2, *v2, *dO;  // fp16 copies
   const float *lse, *delta;
   void *dq, *dk2, *dv2;
   float* band;  // [grid][2 start/end][2 k2/v2][R-1][D]
   int out_f32, R, lR, G, ngroups, items, per_cta, ring;
 };
 
-template <int D>
+template <int D, int RING, bool STAGED>
 struct QSmem {
+  static constexpr int kStages = STAGED ? 2 : 3;
   static constexpr int kPanelBytes = kQChunk * 128;
   static constexpr int kStageBytes = kQChunk * D * 2;
-  alignas(1024) uint8_t k[kQStages][kStageBytes];
-  alignas(1024) uint8_t v[kQStages][kStageBytes];
-  float acc_k2[kRingMax][D];
-  float acc_v2[kRingMax][D];
+  alignas(1024) uint8_t k[kStages][kStageBytes];
+  alignas(1024) uint8_t v[kStages][kStageBytes];
+  float acc_k2[RING][D];
+  float acc_v2[RING][D];
   float eq[128][25], ek[128][25], ev[128][25];
-  uint64_t kvfull[kQStages], kvempty[kQStages];
-  uint64_t sfull, pready, udone, aready;
+  alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D];
+  float slse[2][16], sdl[2][16];
+  uint64_t kvfull[kStages], kvempty[kStages];
+  uint64_t sfull[2], pready[2], udone, aready;
   uint32_t tmem_base;
 };
 
@@ -111,12 +119,32 @@ __device__ __forceinline__ int q_width(const QItem& it, int c) {
   return ((it.span - kQChunk * (it.nch - 1)) + 15) & ~15;
 }
 
+template <int N>
+__device__ __forceinline__ void load_f16(const __half* p, float (&f)[N]) {
+#pragma unroll
+  for (int t = 0; t < N / 8; ++t) {
+    const uint4 x = *reinterpret_cast<const uint4*>(p + 8 * t);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 g = __half22float2(*reinterpret_cast<const __half2*>(&xs[e]));
+      f[8 * t + 2 * e] = g.x;
+      f[8 * t + 2 * e + 1] = g.y;
+    }
+  }
+}
+
+// Row sources of the current tile: staged shared-memory rows or the global fp16 copies.
+struct QRows {
+  const __half *q, *dO, *k2, *v2;  // this thread's rows (valid rows only)
+};
+
 // One epilogue pass over columns [c0, c0+PW) of the tile's W (half 0) / U (half 1) rows:
 // per-row contributions into eq/ek/ev, then reductions into dq (per query) and the dk2/dv2 ring.
-template <int D, int PW, bool DET>
-__device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a, const QItem& it, int c0, int half,
-                                                int r, bool valid, int g, int kpos, uint32_t tW, uint32_t tU,
-                                                int tid256) {
+template <int D, int RING, bool STAGED, int PW, bool DET>
+__device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                                int c0, int half, int r, bool valid, const QRows& rw, uint32_t tW,
+                                                uint32_t tU, int tid256) {
   const Problem& p = a.p;
   const float s = p.scale;
   if (half == 0) {
@@ -131,8 +159,8 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
       for (int e = 0; e < PW; ++e) wv[e] = __uint_as_float(u[e]);
     }
     if (valid) {
-      load_bf16<PW>(a.k2 + p.koff(it.b, kpos, it.h) + c0, k2v);
-      load_bf16<PW>(a.q + p.qoff(it.b, it.i0 + g, it.h) + c0, qv);
+      load_f16<PW>(rw.k2 + c0, k2v);
+      load_f16<PW>(rw.q + c0, qv);
     } else {
 #pragma unroll
       for (int e = 0; e < PW; ++e) k2v[e] = qv[e] = 0.f;
@@ -173,7 +201,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
       for (int e = 0; e < PW; ++e) uv[e] = __uint_as_float(u[e]);
     }
     if (valid) {
-      load_bf16<PW>(a.dO + p.qoff(it.b, it.i0 + g, it.h) + c0, dov);
+      load_f16<PW>(rw.dO + c0, dov);
     } else {
 #pragma unroll
       for (int e = 0; e < PW; ++e) dov[e] = 0.f;
@@ -186,7 +214,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
   for (int idx = tid256; idx < it.nq * PW; idx += 256) {
     const int gq = idx / PW, d = idx % PW;
     float x = 0.f;
-    for (int t = 0; t < a.R; ++t) x += sm.eq[gq * a.R + t][d];
+    for (int t = 0; t < a.R; ++t) x += sm.eq[(gq << a.lR) + t][d];
     const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + d;
     if (a.out_f32)
       reinterpret_cast<float*>(a.dq)[off] = x;
@@ -204,7 +232,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
     float xk = 0.f, xv = 0.f;
     const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
     for (int gg = glo; gg <= ghi; ++gg) {
-      const int row = gg * a.R + (sl - gg);
+      const int row = (gg << a.lR) + (sl - gg);
       xk += sm.ek[row][d];
       xv += sm.ev[row][d];
     }
@@ -216,33 +244,38 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D>& sm, const BwdQArgs& a,
   named_bar_sync(1, 256);
 }
 
-template <int D, bool DET>
+template <int D, bool DET, int RING, bool STAGED>
 __global__ void __launch_bounds__(kQThreads, 1)
     tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
+  using Sm = QSmem<D, RING, STAGED>;
   extern __shared__ uint8_t smem_raw[];
-  static_assert(sizeof(QSmem<D>) + 1024 <= 232448, "shared memory budget");
-  QSmem<D>& sm = *reinterpret_cast<QSmem<D>*>(smem_raw + align1024_pad(smem_raw));
+  static_assert(sizeof(Sm) + 1024 <= 232448, "shared memory budget");
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw + align1024_pad(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kStages = Sm::kStages;
   constexpr int kPanels = D / 64;
-  constexpr uint32_t kPanelBytes = QSmem<D>::kPanelBytes;
+  constexpr uint32_t kPanelBytes = Sm::kPanelBytes;
+  constexpr int kC8 = D / 8;
   const int it_begin = blockIdx.x * a.per_cta;
   const int it_end = min(a.items, it_begin + a.per_cta);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    for (int s = 0; s < kQStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.kvfull[s], 1);
       mbar_init(&sm.kvempty[s], 1);
     }
-    mbar_init(&sm.sfull, 1);
-    mbar_init(&sm.pready, 8);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.sfull[s], 1);
+      mbar_init(&sm.pready[s], 4);
+    }
     mbar_init(&sm.udone, 1);
     mbar_init(&sm.aready, 8);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
-  for (int e = threadIdx.x; e < kRingMax * D; e += kQThreads) {
+  for (int e = threadIdx.x; e < RING * D; e += kQThreads) {
     (&sm.acc_k2[0][0])[e] = 0.f;
     (&sm.acc_v2[0][0])[e] = 0.f;
   }
@@ -258,11 +291,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
       for (int item = it_begin; item < it_end; ++item) {
         QItem it = q_item(a, item);
         for (int c = 0; c < it.nch; ++c, ++kc) {
-          const int s = kc % kQStages;
-          const uint32_t ph = (kc / kQStages) & 1;
+          const int s = kc % kStages;
+          const uint32_t ph = (kc / kStages) & 1;
           const int row = it.jbeg + c * kQChunk;
           mbar_wait(&sm.kvempty[s], ph ^ 1);
-          mbar_expect_tx(&sm.kvfull[s], 2 * QSmem<D>::kStageBytes);
+          mbar_expect_tx(&sm.kvfull[s], 2 * Sm::kStageBytes);
           for (int pn = 0; pn < kPanels; ++pn) {
             tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.h, row, it.b);
             tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.h, row, it.b);
@@ -279,36 +312,49 @@ __global__ void __launch_bounds__(kQThreads, 1)
       uint32_t kc = 0, gc = 0;
       for (int item = it_begin; item < it_end; ++item) {
         QItem it = q_item(a, item);
-        const bool tr = item - it_begin < 3;
+        const bool tr = item - it_begin >= 100 && item - it_begin < 103;
         mbar_wait(&sm.aready, gc & 1);
         tc_fence_after();
         SA_TRACE_POINT(tr, (item - it_begin) << 16 | 10 << 8);
         for (int c = 0; c < it.nch; ++c) {
-          const int s = (kc + c) % kQStages;
-          const uint32_t ph = ((kc + c) / kQStages) & 1;
+          const int s = (kc + c) % kStages;
+          const uint32_t ph = ((kc + c) / kStages) & 1;
           const int w = q_width(it, c);
           mbar_wait(&sm.kvfull[s], ph);
           tc_fence_after();
-          const uint32_t idesc_s = idesc_f16(128, w, 0, 0);
           const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
+          // S / dP for chunk columns [32 hh, 32 hh + 32): each half signals its own barrier
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
-            mma_ts(tS, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-            mma_ts(tdP, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          for (int hh = 0; hh < 2; ++hh) {
+            const int nwh = min(32, w - 32 * hh);
+            if (nwh > 0) {
+              const uint32_t idesc_s = idesc_f16(128, nwh, 0, 0);
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + hh * 32 * 128;
+                mma_ts(tS + 32 * hh, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                mma_ts(tdP + 32 * hh, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s,
+                       kk > 0 ? 1u : 0u);
+              }
+            }
+            mma_commit(&sm.sfull[hh]);
           }
-          mma_commit(&sm.sfull);
           SA_TRACE_POINT(tr, (item - it_begin) << 16 | 11 << 8 | c);
-          mbar_wait(&sm.pready, (kc + c) & 1);
-          tc_fence_after();
-          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 12 << 8 | c);
-          for (int kk = 0; kk < w / 16; ++kk) {
-            const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-            // P / dS of chunk columns [32h, 32h+32) live in TMEM columns [32h, 32h+16) (own region)
-            const uint32_t pc = 32 * (kk >> 1) + 8 * (kk & 1);
-            mma_ts(tW, tdP + pc, smem_desc_sw128(kaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
-            mma_ts(tU, tS + pc, smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_acc, acc);
+          // W += dS K, U += P V, per half as soon as its P / dS are in TMEM
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&sm.pready[hh], (kc + c) & 1);
+            tc_fence_after();
+            const int nwh = min(32, w - 32 * hh);
+            for (int k2i = 0; k2i < nwh / 16; ++k2i) {
+              const uint32_t acc = (c > 0 || hh > 0 || k2i > 0) ? 1u : 0u;
+              const uint32_t roff = (32 * hh + 16 * k2i) * 128;
+              const uint32_t pc = 32 * hh + 8 * k2i;
+              mma_ts(tW, tdP + pc, smem_desc_sw128(kaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
+              mma_ts(tU, tS + pc, smem_desc_sw128(vaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
+            }
           }
+          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 12 << 8 | c);
           mma_commit(&sm.kvempty[s]);
         }
         mma_commit(&sm.udone);
@@ -326,12 +372,55 @@ __global__ void __launch_bounds__(kQThreads, 1)
     const uint32_t tS = tbase + kQS + lane_off, tdP = tbase + kQdP + lane_off;
     const uint32_t tAS = tbase + kQAS + lane_off, tAdP = tbase + kQAdP + lane_off;
     const Problem& p = a.p;
+    const float sl2 = p.scale * kLog2e;
+    // stage tile `item`'s rows into buffer `buf` (cp.async, one group per call)
+    auto stage = [&](int item, int buf) {
+      if (!STAGED) return;
+      const QItem it = q_item(a, item);
+      const int P0 = p.np + it.i0;
+      const int nk = a.R + a.G - 1;
+      const int nrows = 2 * a.G + 2 * nk;
+      for (int task = tid256; task < nrows * kC8; task += 256) {
+        const int row = task / kC8, c8 = task % kC8;
+        const __half* src = nullptr;
+        if (row < a.G) {
+          if (row < it.nq) src = a.q + p.qoff(it.b, it.i0 + row, it.h);
+        } else if (row < 2 * a.G) {
+          if (row - a.G < it.nq) src = a.dO + p.qoff(it.b, it.i0 + row - a.G, it.h);
+        } else {
+          const int rr = row - 2 * a.G;
+          const int kp = P0 - a.R + 1 + (rr < nk ? rr : rr - nk);
+          if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.koff(it.b, kp, it.h);
+        }
+        if (src) cp_async16(&sm.stg[buf][row][8 * c8], src + 8 * c8);
+      }
+      if (tid256 < 2 * it.nq) {
+        const int g = tid256 < it.nq ? tid256 : tid256 - it.nq;
+        const int64_t x = (int64_t(it.b) * p.H + it.h) * p.N + it.i0 + g;
+        if (tid256 < it.nq)
+          cp_async4(&sm.slse[buf][g], a.lse + x);
+        else
+          cp_async4(&sm.sdl[buf][g], a.delta + x);
+      }
+      cp_async_commit();
+    };
     uint32_t kc = 0, gc = 0;
     int PS = 0, flush_lo = 0;
+    if (it_begin < it_end) stage(it_begin, 0);
     for (int item = it_begin; item < it_end; ++item) {
       QItem it = q_item(a, item);
-      const bool tr = threadIdx.x == 128 && item - it_begin < 3;
+      const int buf = STAGED ? int(gc & 1) : 0;
+      const bool tr = threadIdx.x == 128 && item - it_begin >= 100 && item - it_begin < 103;
       SA_TRACE_POINT(tr, (item - it_begin) << 16 | 1 << 8);
+      if (STAGED) {
+        if (item + 1 < it_end) {
+          stage(item + 1, buf ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        named_bar_sync(1, 256);
+      }
       const bool first_in_sub = item == it_begin || it.grp == 0;
       const bool last_in_sub = item == it_end - 1 || it.grp == a.ngroups - 1;
       const int P0 = p.np + it.i0;
@@ -345,23 +434,87 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int kpos = pos - a.R + 1 + kk;
       const bool valid = row_in && kpos >= 0;
       float lse_l2 = 0.f, dl = 0.f;
+      QRows rw{};
       if (row_in) {
-        const int64_t ri = (int64_t(it.b) * p.H + it.h) * p.N + it.i0 + g;
-        lse_l2 = a.lse[ri] * kLog2e;
-        dl = a.delta[ri];
+        if (STAGED) {
+          lse_l2 = sm.slse[buf][g] * kLog2e;
+          dl = sm.sdl[buf][g];
+        } else {
+          const int64_t ri = (int64_t(it.b) * p.H + it.h) * p.N + it.i0 + g;
+          lse_l2 = a.lse[ri] * kLog2e;
+          dl = a.delta[ri];
+        }
       }
-      // ---- row operands: half 0 -> A_S = s (q o k2) [det: s (k2 x q)], half 1 -> A_dP = dO o v2 ----
+      if (valid) {
+        const int nk = a.R + a.G - 1;
+        if (STAGED) {
+          rw.q = &sm.stg[buf][g][0];
+          rw.dO = &sm.stg[buf][a.G + g][0];
+          rw.k2 = &sm.stg[buf][2 * a.G + g + kk][0];
+          rw.v2 = &sm.stg[buf][2 * a.G + nk + g + kk][0];
+        } else {
+          rw.q = a.q + p.qoff(it.b, it.i0 + g, it.h);
+          rw.dO = a.dO + p.qoff(it.b, it.i0 + g, it.h);
+          rw.k2 = a.k2 + p.koff(it.b, kpos, it.h);
+          rw.v2 = a.v2 + p.koff(it.b, kpos, it.h);
+        }
+      }
+      // ---- row operands (fp16, unscaled): half 0 -> A_S = q o k2 [det: k2 x q], half 1 -> A_dP = dO o v2 ----
       {
         uint32_t pk[D / 2];
 #pragma unroll
         for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
         if (valid) {
-          if (half == 0)
-            row_operand_f16<D>(a.q + p.qoff(it.b, it.i0 + g, it.h), a.k2 + p.koff(it.b, kpos, it.h), p.scale, DET,
-                               pk);
-          else
-            row_operand_f16<D>(a.dO + p.qoff(it.b, it.i0 + g, it.h), a.v2 + p.koff(it.b, kpos, it.h), 1.f, false,
-                               pk);
+          const __half* x = half == 0 ? rw.q : rw.dO;
+          const __half* y = half == 0 ? rw.k2 : rw.v2;
+          if (DET && half == 0) {
+            constexpr int D3 = (D / 3) * 3;
+#pragma unroll
+            for (int base = 0; base < D; base += 24) {
+              float xf[24], yf[24];
+#pragma unroll
+              for (int u = 0; u < 3; ++u) {
+                if (base + 8 * u < D) {
+                  float tx[8], ty[8];
+                  load_f16<8>(x + base + 8 * u, tx);
+                  load_f16<8>(y + base + 8 * u, ty);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    xf[8 * u + e] = tx[e];
+                    yf[8 * u + e] = ty[e];
+                  }
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
+                }
+              }
+#pragma unroll
+              for (int c3 = 0; c3 < 24; c3 += 3) {
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+                if (base + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
+                  a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+                  a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+                  a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+                }
+                xf[c3] = a0;
+                xf[c3 + 1] = a1;
+                xf[c3 + 2] = a2;
+              }
+#pragma unroll
+              for (int e = 0; e < 24; e += 2)
+                if (base + e < D) pk[(base + e) / 2] = pack_f16x2(xf[e], xf[e + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < D / 8; ++t) {
+              const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * t);
+              const uint4 yv = *reinterpret_cast<const uint4*>(y + 8 * t);
+              pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
+              pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
+              pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
+              pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
+            }
+          }
         }
         tmem_store_row<D>(half == 0 ? tAS : tAdP, pk);
         tmem_st_wait();
@@ -370,13 +523,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
         if (lane == 0) mbar_arrive(&sm.aready);
         SA_TRACE_POINT(tr, (item - it_begin) << 16 | 2 << 8);
       }
-      // ---- chunks: P = exp(S - lse), dS = P (dP - delta) ----
+      // ---- chunks: P = exp(S - lse), dS = P (dP - delta), this half's 32 columns ----
       const int jlo = max(0, pos - p.w1 + 1);
       for (int c = 0; c < it.nch; ++c) {
         const int w = q_width(it, c);
         const int cb = 32 * half;
         const int nw = max(0, min(32, w - cb));
-        mbar_wait(&sm.sfull, (kc + c) & 1);
+        mbar_wait(&sm.sfull[half], (kc + c) & 1);
         tc_fence_after();
         SA_TRACE_POINT(tr, (item - it_begin) << 16 | 3 << 8 | c);
         if (nw > 0) {
@@ -400,16 +553,16 @@ __global__ void __launch_bounds__(kQThreads, 1)
           if (!__any_sync(0xffffffffu, need_mask)) {
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-              const float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), kLog2e, -lse_l2));
-              const float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), kLog2e, -lse_l2));
+              const float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), sl2, -lse_l2));
+              const float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), sl2, -lse_l2));
               pp[t] = pack_f16x2(p0, p1);
               pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
             }
           } else {
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-              float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), kLog2e, -lse_l2));
-              float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), kLog2e, -lse_l2));
+              float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), sl2, -lse_l2));
+              float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), sl2, -lse_l2));
               p0 = (2 * t >= lo_c && 2 * t <= hi_c) ? p0 : 0.f;
               p1 = (2 * t + 1 >= lo_c && 2 * t + 1 <= hi_c) ? p1 : 0.f;
               pp[t] = pack_f16x2(p0, p1);
@@ -417,17 +570,17 @@ __global__ void __launch_bounds__(kQThreads, 1)
             }
           }
           if (nw == 32) {
-            tmem_st16(tS + 32 * half, pp);
-            tmem_st16(tdP + 32 * half, pd);
+            tmem_st16(tS + cb, pp);
+            tmem_st16(tdP + cb, pd);
           } else {
-            tmem_st8(tS + 32 * half, pp);
-            tmem_st8(tdP + 32 * half, pd);
+            tmem_st8(tS + cb, pp);
+            tmem_st8(tdP + cb, pd);
           }
           tmem_st_wait();
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pready);
+        if (lane == 0) mbar_arrive(&sm.pready[half]);
         SA_TRACE_POINT(tr, (item - it_begin) << 16 | 4 << 8 | c);
       }
       // ---- epilogue ----
@@ -437,13 +590,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (DET) {
 #pragma unroll 1
         for (int c0 = 0; c0 + 24 <= D; c0 += 24)
-          q_epilogue_pass<D, 24, DET>(sm, a, it, c0, half, r, valid, g, kpos, tW, tU, tid256);
+          q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
         if constexpr (D % 24 != 0)
-          q_epilogue_pass<D, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, g, kpos, tW, tU, tid256);
+          q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256);
       } else {
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 16)
-          q_epilogue_pass<D, 16, DET>(sm, a, it, c0, half, r, valid, g, kpos, tW, tU, tid256);
+          q_epilogue_pass<D, RING, STAGED, 16, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
       }
       tc_fence_before();
       SA_TRACE_POINT(tr, (item - it_begin) << 16 | 6 << 8);
@@ -581,10 +734,6 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int c8) {
   return uint32_t((c8 >> 3) * (128 * 128) + row * 128 + (((c8 & 7) ^ (row & 7)) << 4));
 }
 
-__device__ __forceinline__ uint32_t hmul2_u32(uint32_t x, uint32_t y) {
-  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&x), *reinterpret_cast<__half2*>(&y));
-  return *reinterpret_cast<uint32_t*>(&r);
-}
 
 template <int D, bool DET, bool STAGED>
 __global__ void __launch_bounds__(kKVThreads, 1)
@@ -1053,10 +1202,10 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
       return cudaErrorInvalidValue;
     BwdQArgs a;
     a.p = p;
-    a.q = (const __nv_bfloat16*)q;
-    a.k2 = (const __nv_bfloat16*)k2;
-    a.v2 = (const __nv_bfloat16*)v2;
-    a.dO = (const __nv_bfloat16*)dO;
+    a.q = (const __half*)qf;
+    a.k2 = (const __half*)k2f;
+    a.v2 = (const __half*)v2f;
+    a.dO = (const __half*)dof;
     a.lse = lse;
     a.delta = delta;
     a.dq = dq;
@@ -1075,17 +1224,21 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
       KernelScope ks("tc_bwd_q", st);
       kern<<<grid, kQThreads, smem, st>>>(tmK, tmV, a);
     };
+    // staged rows: q, dO (G each) + k2, v2 (R+G-1 each) double-buffered; the ring holds R+G rows
+    const bool staged = G <= 16 && 2 * G + 2 * (R + G - 1) <= kQStageRows && R + G <= 36;
+#define SA_Q_LAUNCH(DD, DET, RING, STG) launch(tc_bwd_q_kernel<DD, DET, RING, STG>, sizeof(QSmem<DD, RING, STG>) + 1024)
     if (p.D == 128) {
       if (p.det)
-        launch(tc_bwd_q_kernel<128, true>, sizeof(QSmem<128>) + 1024);
+        staged ? SA_Q_LAUNCH(128, true, 36, true) : SA_Q_LAUNCH(128, true, 66, false);
       else
-        launch(tc_bwd_q_kernel<128, false>, sizeof(QSmem<128>) + 1024);
+        staged ? SA_Q_LAUNCH(128, false, 36, true) : SA_Q_LAUNCH(128, false, 66, false);
     } else {
       if (p.det)
-        launch(tc_bwd_q_kernel<64, true>, sizeof(QSmem<64>) + 1024);
+        staged ? SA_Q_LAUNCH(64, true, 36, true) : SA_Q_LAUNCH(64, true, 66, false);
       else
-        launch(tc_bwd_q_kernel<64, false>, sizeof(QSmem<64>) + 1024);
+        staged ? SA_Q_LAUNCH(64, false, 36, true) : SA_Q_LAUNCH(64, false, 66, false);
     }
+#undef SA_Q_LAUNCH
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     KernelScope ks("tc_fold", st);
