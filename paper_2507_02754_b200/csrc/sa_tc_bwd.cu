@@ -81,7 +81,7 @@ struct BwdQArgs {
 
 template <int D, int RING, bool STAGED>
 struct QSmem {
-  static constexpr int kStages = STAGED ? 2 : 3;
+  static constexpr int kStages = 3;
   static constexpr int kPanelBytes = kQChunk * 128;
   static constexpr int kStageBytes = kQChunk * D * 2;
   alignas(1024) uint8_t k[kStages][kStageBytes];
@@ -89,7 +89,8 @@ struct QSmem {
   float acc_k2[RING][D];
   float acc_v2[RING][D];
   float eq[128][25], ek[128][25], ev[128][25];
-  alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D];
+  // staged rows; pitch D+8 halves so that lanes reading consecutive rows hit distinct banks
+  alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D + 8];
   float slse[2][16], sdl[2][16];
   uint64_t kvfull[kStages], kvempty[kStages];
   uint64_t sfull[2], pready[2], udone, aready;
@@ -210,16 +211,32 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     for (int e = 0; e < PW; ++e) sm.ev[r][e] = dov[e] * uv[e];
   }
   named_bar_sync(1, 256);
-  // dq: sum over the R rows of each query
-  for (int idx = tid256; idx < it.nq * PW; idx += 256) {
-    const int gq = idx / PW, d = idx % PW;
-    float x = 0.f;
-    for (int t = 0; t < a.R; ++t) x += sm.eq[(gq << a.lR) + t][d];
-    const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + d;
-    if (a.out_f32)
-      reinterpret_cast<float*>(a.dq)[off] = x;
-    else
-      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(x);
+  // dq: sum over the R rows of each query; 4 lanes per output, rows interleaved, shuffle-combined
+  for (int base = 0; base < it.nq * PW * 4; base += 256) {
+    const int idx = base + tid256;
+    const bool act = idx < it.nq * PW * 4;
+    const int o = idx >> 2, part = idx & 3;
+    const int gq = o / PW, d = o % PW;
+    float x0 = 0.f, x1 = 0.f;
+    if (act) {
+      const float(*rows)[25] = sm.eq + (gq << a.lR);
+      int t = part;
+      for (; t + 4 < a.R; t += 8) {
+        x0 += rows[t][d];
+        x1 += rows[t + 4][d];
+      }
+      if (t < a.R) x0 += rows[t][d];
+    }
+    float x = x0 + x1;
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    if (act && part == 0) {
+      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + d;
+      if (a.out_f32)
+        reinterpret_cast<float*>(a.dq)[off] = x;
+      else
+        reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(x);
+    }
   }
   // dk2 / dv2: key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g)
   const int P0 = p.np + it.i0;
