@@ -210,7 +210,9 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
 #pragma unroll
     for (int e = 0; e < PW; ++e) sm.ev[r][e] = dov[e] * uv[e];
   }
+  SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 20 << 8 | c0);
   named_bar_sync(1, 256);
+  SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 21 << 8 | c0);
   // dq: sum over the R rows of each query; 4 lanes per output, rows interleaved, shuffle-combined
   for (int base = 0; base < it.nq * PW * 4; base += 256) {
     const int idx = base + tid256;
@@ -258,6 +260,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     sm.acc_k2[slot][c0 + d] += xk;
     sm.acc_v2[slot][c0 + d] += xv;
   }
+  SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 22 << 8 | c0);
   named_bar_sync(1, 256);
 }
 
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = sm.tmem_base;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
-    if (lane == 0) {
+    {  // whole warp; elected lane issues
       const uint32_t tW = tbase + kQW, tU = tbase + kQU, tS = tbase + kQS, tdP = tbase + kQdP;
       const uint32_t tAS = tbase + kQAS, tAdP = tbase + kQAdP;
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const bool tr = item - it_begin >= 100 && item - it_begin < 103;
         mbar_wait(&sm.aready, gc & 1);
         tc_fence_after();
-        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 10 << 8);
+        SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 10 << 8);
         for (int c = 0; c < it.nch; ++c) {
           const int s = (kc + c) % kStages;
           const uint32_t ph = ((kc + c) / kStages) & 1;
@@ -349,14 +352,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + hh * 32 * 128;
-                mma_ts(tS + 32 * hh, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                mma_ts(tdP + 32 * hh, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s,
+                mma_ts_w(tS + 32 * hh, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                mma_ts_w(tdP + 32 * hh, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s,
                        kk > 0 ? 1u : 0u);
               }
             }
-            mma_commit(&sm.sfull[hh]);
+            mma_commit_w(&sm.sfull[hh]);
           }
-          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 11 << 8 | c);
+          SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 11 << 8 | c);
           // W += dS K, U += P V, per half as soon as its P / dS are in TMEM
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -367,14 +370,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
               const uint32_t acc = (c > 0 || hh > 0 || k2i > 0) ? 1u : 0u;
               const uint32_t roff = (32 * hh + 16 * k2i) * 128;
               const uint32_t pc = 32 * hh + 8 * k2i;
-              mma_ts(tW, tdP + pc, smem_desc_sw128(kaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
-              mma_ts(tU, tS + pc, smem_desc_sw128(vaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
+              mma_ts_w(tW, tdP + pc, smem_desc_sw128(kaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
+              mma_ts_w(tU, tS + pc, smem_desc_sw128(vaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
             }
           }
-          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 12 << 8 | c);
-          mma_commit(&sm.kvempty[s]);
+          SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 12 << 8 | c);
+          mma_commit_w(&sm.kvempty[s]);
         }
-        mma_commit(&sm.udone);
+        mma_commit_w(&sm.udone);
         kc += it.nch;
         ++gc;
       }
@@ -787,7 +790,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = sm.tmem_base;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
   if (warp == 0 || warp == 2 || warp == 3) {
     // ------------------------------ TMA (once) + A-tile formers ------------------------------
@@ -969,7 +972,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
-    if (lane == 0 && ntile > 0) {
+    if (ntile > 0) {  // whole warp; elected lane issues
       const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
       const uint32_t idesc_s = idesc_f16(128, 64, 0, 0);
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
@@ -986,12 +989,12 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
             const uint32_t boff = off + hh * 64 * 128;
-            mma_ss(tST + 64 * hh, smem_desc_sw128(kaddr + off, 16, 1024), smem_desc_sw128(asa + boff, 16, 1024),
+            mma_ss_w(tST + 64 * hh, smem_desc_sw128(kaddr + off, 16, 1024), smem_desc_sw128(asa + boff, 16, 1024),
                    idesc_s, kk > 0 ? 1u : 0u);
-            mma_ss(tdPT + 64 * hh, smem_desc_sw128(vaddr + off, 16, 1024), smem_desc_sw128(ada + boff, 16, 1024),
+            mma_ss_w(tdPT + 64 * hh, smem_desc_sw128(vaddr + off, 16, 1024), smem_desc_sw128(ada + boff, 16, 1024),
                    idesc_s, kk > 0 ? 1u : 0u);
           }
-          mma_commit(&sm.sfull[hh]);
+          mma_commit_w(&sm.sfull[hh]);
         }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -1001,13 +1004,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t acc = (t > 0 || hh > 0 || kk > 0) ? 1u : 0u;
             const uint32_t roff = (64 * hh + 16 * kk) * 128;
-            mma_ts(tdV, tST + 64 * hh + 8 * kk, smem_desc_sw128(ada + roff, kPanelBytes, 1024), idesc_acc, acc);
-            mma_ts(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
+            mma_ts_w(tdV, tST + 64 * hh + 8 * kk, smem_desc_sw128(ada + roff, kPanelBytes, 1024), idesc_acc, acc);
+            mma_ts_w(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
           }
         }
-        mma_commit(&sm.afree[buf]);
+        mma_commit_w(&sm.afree[buf]);
       }
-      mma_commit(&sm.done);
+      mma_commit_w(&sm.done);
     }
   } else if (warp >= 4) {
     // ------------------------------ P^T, dS^T and the dK/dV epilogue ------------------------------

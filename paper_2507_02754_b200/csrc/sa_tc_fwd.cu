@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = sm.tmem_base;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
-    if (lane == 0) {
+    {  // whole warp; elected lane issues
       const uint32_t tU = tbase + kColU, tA = tbase + kColA;
       const uint32_t tS[2] = {tbase + kColS0, tbase + kColS1};
       const uint32_t idesc_pv = idesc_f16(128, D, 0, 1);
@@ -168,10 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t vaddr = smem_u32(sm.v[s]);
           for (int kk = 0; kk < w / 16; ++kk) {
             uint64_t bd = smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024);
-            mma_ts(tU, tS[sb] + kk * 8, bd, idesc_pv, (c > 0 || kk > 0) ? 1u : 0u);
+            mma_ts_w(tU, tS[sb] + kk * 8, bd, idesc_pv, (c > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&sm.vempty[s]);
-          mma_commit(&sm.pvdone);
+          mma_commit_w(&sm.vempty[s]);
+          mma_commit_w(&sm.pvdone);
         };
         for (int c = 0; c < it.nch; ++c) {
           const int s = (kc + c) % kStages;
@@ -184,14 +184,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             uint64_t bd = smem_desc_sw128(kaddr + (kk / 4) * kPanelBytes + (kk % 4) * 32, 16, 1024);
-            mma_ts(tS[sb], tA + kk * 8, bd, idesc_s, kk > 0 ? 1u : 0u);
+            mma_ts_w(tS[sb], tA + kk * 8, bd, idesc_s, kk > 0 ? 1u : 0u);
           }
-          mma_commit(&sm.sfull[sb]);
-          mma_commit(&sm.kempty[s]);
+          mma_commit_w(&sm.sfull[sb]);
+          mma_commit_w(&sm.kempty[s]);
           if (c > 0) issue_pv(c - 1);
         }
         issue_pv(it.nch - 1);
-        mma_commit(&sm.udone);
+        mma_commit_w(&sm.udone);
         kc += it.nch;
         cc += it.nch;
         pvc += it.nch;
