@@ -336,31 +336,38 @@ __global__ void __launch_bounds__(kQThreads, 1)
         mbar_wait(&sm.aready, gc & 1);
         tc_fence_after();
         SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 10 << 8);
+        // Issue order per chunk c and half hh (hh = column halves [32hh, 32hh+32) of a 64-row chunk):
+        //   S_hh(0), dP_hh(0) ... then for each c: [P_hh(c) ready] W_hh(c), U_hh(c); S_hh(c+1), dP_hh(c+1)
+        // so half a's next S overlaps half b's softmax (the tensor pipe is in-order, so S_hh(c+1)
+        // overwriting the TMEM that held P_hh(c) / dS_hh(c) follows the W/U MMAs that read them).
+        auto issue_s = [&](int c, int hh) {
+          const int s = (kc + c) % kStages;
+          const int w = q_width(it, c);
+          const int nwh = min(32, w - 32 * hh);
+          if (nwh > 0) {
+            const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
+            const uint32_t idesc_s = idesc_f16(128, nwh, 0, 0);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + hh * 32 * 128;
+              mma_ts_w(tS + 32 * hh, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+              mma_ts_w(tdP + 32 * hh, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s,
+                       kk > 0 ? 1u : 0u);
+            }
+          }
+          mma_commit_w(&sm.sfull[hh]);
+        };
+        {
+          mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
+          tc_fence_after();
+          issue_s(0, 0);
+          issue_s(0, 1);
+        }
         for (int c = 0; c < it.nch; ++c) {
           const int s = (kc + c) % kStages;
-          const uint32_t ph = ((kc + c) / kStages) & 1;
           const int w = q_width(it, c);
-          mbar_wait(&sm.kvfull[s], ph);
-          tc_fence_after();
           const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
-          // S / dP for chunk columns [32 hh, 32 hh + 32): each half signals its own barrier
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int nwh = min(32, w - 32 * hh);
-            if (nwh > 0) {
-              const uint32_t idesc_s = idesc_f16(128, nwh, 0, 0);
-#pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
-                const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + hh * 32 * 128;
-                mma_ts_w(tS + 32 * hh, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                mma_ts_w(tdP + 32 * hh, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s,
-                       kk > 0 ? 1u : 0u);
-              }
-            }
-            mma_commit_w(&sm.sfull[hh]);
-          }
           SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 11 << 8 | c);
-          // W += dS K, U += P V, per half as soon as its P / dS are in TMEM
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             mbar_wait(&sm.pready[hh], (kc + c) & 1);
@@ -372,6 +379,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
               const uint32_t pc = 32 * hh + 8 * k2i;
               mma_ts_w(tW, tdP + pc, smem_desc_sw128(kaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
               mma_ts_w(tU, tS + pc, smem_desc_sw128(vaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
+            }
+            if (c + 1 < it.nch) {
+              if (hh == 0) {
+                mbar_wait(&sm.kvfull[(kc + c + 1) % kStages], ((kc + c + 1) / kStages) & 1);
+                tc_fence_after();
+              }
+              issue_s(c + 1, hh);
             }
           }
           SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 12 << 8 | c);
