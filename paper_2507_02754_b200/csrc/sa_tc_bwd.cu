@@ -183,6 +183,34 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
           for (int e = t; e < t + 3 && e < PW; ++e) sm.eq[r][e] = sm.ek[r][e] = 0.f;
         }
       }
+    } else if (PW == 16 && a.R == 32) {
+      // R = 32: the warp holds exactly one query's rows -> dq by a register reduce-scatter
+      float v[16];
+#pragma unroll
+      for (int e = 0; e < PW; ++e) {
+        v[e & 15] = s * k2v[e] * wv[e];
+        sm.ek[r][e] = s * qv[e] * wv[e];
+      }
+      const int ln = r & 31;
+#pragma unroll
+      for (int st = 16, n = 8; st >= 2; st >>= 1, n >>= 1) {
+        const bool hi = ln & st;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+        }
+      }
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+      const int gq = r >> 5;
+      if ((ln & 1) == 0 && gq < it.nq) {
+        const int col = ((ln >> 4) & 1) * 8 + ((ln >> 3) & 1) * 4 + ((ln >> 2) & 1) * 2 + ((ln >> 1) & 1);
+        const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + col;
+        if (a.out_f32)
+          reinterpret_cast<float*>(a.dq)[off] = v[0];
+        else
+          reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+      }
     } else {
 #pragma unroll
       for (int e = 0; e < PW; ++e) {
@@ -214,7 +242,8 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
   named_bar_sync(1, 256);
   SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 21 << 8 | c0);
   // dq: sum over the R rows of each query; 4 lanes per output, rows interleaved, shuffle-combined
-  for (int base = 0; base < it.nq * PW * 4; base += 256) {
+  const bool dq_done = !DET && PW == 16 && a.R == 32;
+  for (int base = 0; !dq_done && base < it.nq * PW * 4; base += 256) {
     const int idx = base + tid256;
     const bool act = idx < it.nq * PW * 4;
     const int o = idx >> 2, part = idx & 3;
@@ -250,10 +279,17 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     if (kp < 0) continue;
     float xk = 0.f, xv = 0.f;
     const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
-    for (int gg = glo; gg <= ghi; ++gg) {
-      const int row = (gg << a.lR) + (sl - gg);
-      xk += sm.ek[row][d];
-      xv += sm.ev[row][d];
+    for (int g0 = glo; g0 <= ghi; g0 += 4) {
+      float tk[4], tv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // independent loads first, then the sums
+        const int gg = g0 + u;
+        const int row = (gg << a.lR) + (sl - gg);
+        tk[u] = gg <= ghi ? sm.ek[row][d] : 0.f;
+        tv[u] = gg <= ghi ? sm.ev[row][d] : 0.f;
+      }
+      xk += (tk[0] + tk[1]) + (tk[2] + tk[3]);
+      xv += (tv[0] + tv[1]) + (tv[2] + tv[3]);
     }
     int slot = sbase + sl;  // (P0 - R + 1 + sl) mod ring
     if (slot >= a.ring) slot -= a.ring;
