@@ -908,7 +908,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         named_bar_sync(2, kNF);
       }
+      const bool trf = ft == 0 && t >= 50 && t < 53;
+      SA_TRACE_POINT(trf, t << 16 | 30 << 8);
       mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
+      SA_TRACE_POINT(trf, t << 16 | 31 << 8);
       // row info: (lse * log2e, delta), +inf marks rows outside the problem
       const int kbase = p.np + q0 - a.R + 1;  // key row of tile row 0
       const int sbase = STAGED ? ring_mod(kbase) : 0;
@@ -932,6 +935,51 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kWS = DET ? 24 : 8;       // A_S task width (elements)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
+      if (!DET) {
+        // trilinear: 4 independent (row, chunk) tasks per iteration, all shared-memory loads first
+        constexpr int kU = 4;
+        for (int t0 = ft; t0 < 128 * kC8; t0 += kU * kNF) {
+          uint4 xq[kU], yk[kU], ud[kU], wv[kU];
+          uint32_t dst[kU];
+          bool ok[kU], in[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int task = t0 + u * kNF;
+            in[u] = task < 128 * kC8;
+            const int r = task / kC8, tk = task % kC8;
+            const int g = r >> a.lR, kk = r & (a.R - 1);
+            const int i = q0 + g;
+            const int kpos = kbase + g + kk;
+            ok[u] = in[u] && r < a.G * a.R && i < qb && kpos >= 0;
+            int slot = sbase + g + kk;
+            if (slot >= a.ring) slot -= a.ring;
+            dst[u] = sw128_off(r, tk);
+            if (ok[u]) {
+              const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
+              const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
+              const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
+              const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
+              xq[u] = *reinterpret_cast<const uint4*>(qrow + 8 * tk);
+              yk[u] = *reinterpret_cast<const uint4*>(k2row + 8 * tk);
+              ud[u] = *reinterpret_cast<const uint4*>(dorow + 8 * tk);
+              wv[u] = *reinterpret_cast<const uint4*>(v2row + 8 * tk);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (!in[u]) continue;
+            uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
+            if (ok[u]) {
+              oa = make_uint4(hmul2_u32(xq[u].x, yk[u].x), hmul2_u32(xq[u].y, yk[u].y), hmul2_u32(xq[u].z, yk[u].z),
+                              hmul2_u32(xq[u].w, yk[u].w));
+              od = make_uint4(hmul2_u32(ud[u].x, wv[u].x), hmul2_u32(ud[u].y, wv[u].y), hmul2_u32(ud[u].z, wv[u].z),
+                              hmul2_u32(ud[u].w, wv[u].w));
+            }
+            *reinterpret_cast<uint4*>(sm.as[buf] + dst[u]) = oa;
+            *reinterpret_cast<uint4*>(sm.adp[buf] + dst[u]) = od;
+          }
+        }
+      } else
       for (int task = ft; task < 128 * kTasks; task += kNF) {
         const int r = task / kTasks, tk = task % kTasks;
         const int g = r >> a.lR, kk = r & (a.R - 1);
@@ -1018,6 +1066,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.aready[buf]);
+      SA_TRACE_POINT(trf, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
   } else if (warp == 1) {
@@ -1032,6 +1081,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int buf = t & 1;
         mbar_wait(&sm.aready[buf], (t >> 1) & 1);
         tc_fence_after();
+        const bool trm = lane == 0 && t >= 50 && t < 53;
+        SA_TRACE_POINT(trm, t << 16 | 40 << 8);
         const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -1058,6 +1109,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             mma_ts_w(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
           }
         }
+        SA_TRACE_POINT(trm, t << 16 | 41 << 8);
         mma_commit_w(&sm.afree[buf]);
       }
       mma_commit_w(&sm.done);
@@ -1075,8 +1127,11 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
       const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
+      const bool trs = threadIdx.x == 128 + 128 * half && t >= 50 && t < 53;
+      SA_TRACE_POINT(trs, t << 16 | (50 + half) << 8);
       mbar_wait(&sm.sfull[half], t & 1);
       tc_fence_after();
+      SA_TRACE_POINT(trs, t << 16 | (52 + half) << 8);
       uint32_t su[64], du[64];
       tmem_ld32(tST + cb, *reinterpret_cast<uint32_t(*)[32]>(su));
       tmem_ld32(tST + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(su + 32));
@@ -1116,6 +1171,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.pready[half]);
+      SA_TRACE_POINT(trs, t << 16 | (54 + half) << 8);
     }
     // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns; dK carries the scale s
     if (ntile > 0) {
