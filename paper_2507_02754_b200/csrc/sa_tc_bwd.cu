@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(256) delta_kernel(Problem p, const __nv_bfloat
 // ==========================================================================================
 // bwd_q: dQ, dK2, dV2
 // ==========================================================================================
-constexpr int kQThreads = 384;
+constexpr int kQThreads = 320;
+constexpr int kQWarpTMA = 8, kQWarpMMA = 9;  // compute warps 0-7 (see tc_fwd: high ids win issue)
 constexpr int kQChunk = 64;
 // TMEM columns
 constexpr uint32_t kQW = 0, kQU = 128, kQS = 256, kQdP = 320, kQAS = 384, kQAdP = 448;
@@ -238,9 +239,9 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
 #pragma unroll
     for (int e = 0; e < PW; ++e) sm.ev[r][e] = dov[e] * uv[e];
   }
-  SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 20 << 8 | c0);
+  SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 20 << 8 | c0);
   named_bar_sync(1, 256);
-  SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 21 << 8 | c0);
+  SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 21 << 8 | c0);
   // dq: sum over the R rows of each query; 4 lanes per output, rows interleaved, shuffle-combined
   const bool dq_done = !DET && PW == 16 && a.R == 32;
   for (int base = 0; !dq_done && base < it.nq * PW * 4; base += 256) {
@@ -296,7 +297,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     sm.acc_k2[slot][c0 + d] += xk;
     sm.acc_v2[slot][c0 + d] += xv;
   }
-  SA_TRACE_POINT(threadIdx.x == 128 && it.grp == 100, 22 << 8 | c0);
+  SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 22 << 8 | c0);
   named_bar_sync(1, 256);
 }
 
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   const int it_begin = blockIdx.x * a.per_cta;
   const int it_end = min(a.items, it_begin + a.per_cta);
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kQWarpTMA && lane == 0) {
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     for (int s = 0; s < kStages; ++s) {
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     mbar_init(&sm.aready, 8);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == kQWarpMMA) tmem_alloc<512>(&sm.tmem_base);
   for (int e = threadIdx.x; e < RING * D; e += kQThreads) {
     (&sm.acc_k2[0][0])[e] = 0.f;
     (&sm.acc_v2[0][0])[e] = 0.f;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
-  if (warp == 0) {
+  if (warp == kQWarpTMA) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       uint32_t kc = 0;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kQWarpMMA) {
     // ------------------------------ MMA issuer ------------------------------
     {  // whole warp; elected lane issues
       const uint32_t tW = tbase + kQW, tU = tbase + kQU, tS = tbase + kQS, tdP = tbase + kQdP;
@@ -432,11 +433,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
         ++gc;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ------------------------------ softmax-gradient + epilogue ------------------------------
-    const int qd = warp & 3, half = (warp - 4) >> 2;
+    const int qd = warp & 3, half = warp >> 2;
     const int r = qd * 32 + lane;
-    const int tid256 = threadIdx.x - 128;
+    const int tid256 = threadIdx.x;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t tW = tbase + kQW + lane_off, tU = tbase + kQU + lane_off;
     const uint32_t tS = tbase + kQS + lane_off, tdP = tbase + kQdP + lane_off;
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     for (int item = it_begin; item < it_end; ++item) {
       QItem it = q_item(a, item);
       const int buf = STAGED ? int(gc & 1) : 0;
-      const bool tr = threadIdx.x == 128 && item - it_begin >= 100 && item - it_begin < 103;
+      const bool tr = threadIdx.x == 0 && item - it_begin >= 100 && item - it_begin < 103;
       SA_TRACE_POINT(tr, (item - it_begin) << 16 | 1 << 8);
       if (STAGED) {
         if (item + 1 < it_end) {
@@ -716,7 +717,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
 
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_free<512>(tbase);
+  if (warp == kQWarpMMA) tmem_free<512>(tbase);
 }
 
 // Band fold: key rows shared by two consecutive CTA ranges get both partial sums; prefix rows no
@@ -767,7 +768,7 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
 // exponent and the dK epilogue) are formed by 3 former warps from an fp16 staging ring filled
 // with cp.async one tile ahead.
 // ==========================================================================================
-constexpr int kKVThreads = 384;
+constexpr int kKVThreads = 384;  // warps 0-7 softmax-gradient, 8-10 A-tile formers (8 also TMA), 11 MMA
 constexpr uint32_t kKST = 0, kKdPT = 128, kKdV = 256, kKdK = 384;
 constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
 constexpr int kKVGmax = 8;    // staged queries per tile
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   const int qb = min(j0 + 128 + p.w1 - 1, p.np + p.N) - p.np;
   const int ntile = qb > qa ? (qb - qa + a.G - 1) / a.G : 0;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(&sm.kvload, 1);
@@ -836,22 +837,22 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     mbar_init(&sm.done, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 11) tmem_alloc<512>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
-  if (warp == 0 || warp == 2 || warp == 3) {
+  if (warp >= 8 && warp <= 10) {
     // ------------------------------ TMA (once) + A-tile formers ------------------------------
-    if (warp == 0 && lane == 0 && ntile > 0) {
+    if (warp == 8 && lane == 0 && ntile > 0) {
       mbar_expect_tx(&sm.kvload, 2 * KVSmem<D>::kTileBytes);
       for (int pn = 0; pn < kPanels; ++pn) {
         tma_load_4d(sm.kb + pn * kPanelBytes, &tmK, &sm.kvload, pn * 64, h, j0, b);
         tma_load_4d(sm.vb + pn * kPanelBytes, &tmV, &sm.kvload, pn * 64, h, j0, b);
       }
     }
-    const int ft = (warp == 0 ? 0 : warp - 1) * 32 + lane;  // 0..95
+    const int ft = (warp - 8) * 32 + lane;  // 0..95
     constexpr int kNF = 96;
     // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
     auto ring_mod = [&](int kp) {  // kp mod ring for kp >= -ring (one division per call site)
@@ -1069,7 +1070,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       SA_TRACE_POINT(trf, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
-  } else if (warp == 1) {
+  } else if (warp == 11) {
     // ------------------------------ MMA issuer ------------------------------
     if (ntile > 0) {  // whole warp; elected lane issues
       const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
@@ -1114,9 +1115,9 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       mma_commit_w(&sm.done);
     }
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ------------------------------ P^T, dS^T and the dK/dV epilogue ------------------------------
-    const int qd = warp & 3, half = (warp - 4) >> 2;
+    const int qd = warp & 3, half = warp >> 2;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t tST = tbase + kKST + lane_off, tdPT = tbase + kKdPT + lane_off;
     const uint32_t tdV = tbase + kKdV + lane_off, tdK = tbase + kKdK + lane_off;
@@ -1127,7 +1128,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
       const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
-      const bool trs = threadIdx.x == 128 + 128 * half && t >= 50 && t < 53;
+      const bool trs = threadIdx.x == 128 * half && t >= 50 && t < 53;
       SA_TRACE_POINT(trs, t << 16 | (50 + half) << 8);
       mbar_wait(&sm.sfull[half], t & 1);
       tc_fence_after();
@@ -1227,7 +1228,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_free<512>(tbase);
+  if (warp == 11) tmem_free<512>(tbase);
 }
 
 }  // namespace

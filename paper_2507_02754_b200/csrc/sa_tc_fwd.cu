@@ -11,10 +11,10 @@
 // P:241-244).  K and V tiles arrive by TMA (128B swizzle) into a 3-stage ring; all MMAs use fp16
 // operands with fp32 accumulation (K/V converted from bf16 exactly by a pre-pass).
 //
-// Warp roles (384 threads, 1 CTA/SM, persistent over (b,h,tile) items):
-//   warp 0: TMA producer;  warp 1: TMEM allocator + single-thread MMA issuer;
-//   warps 4-11: row softmax + epilogue; warps 4+q and 8+q own TMEM lanes 32q..32q+31 and split
-//   each S chunk's columns in two halves (max exchanged through shared memory).
+// Warp roles (320 threads, 1 CTA/SM, persistent over (b,h,tile) items):
+//   warps 0-7: row softmax + epilogue; warps q and 4+q own TMEM lanes 32q..32q+31 and split each S
+//   chunk's columns in two halves (max exchanged through shared memory); warp 8: TMA producer;
+//   warp 9: TMEM allocator + MMA issuer (whole warp, one elected lane issues).
 #include <math.h>
 
 #include <algorithm>
@@ -32,7 +32,10 @@ namespace {
 
 using namespace tc;
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 320;
+// warp roles: 0-7 softmax/epilogue (low ids: the scheduler favours high ids, so the latency-critical
+// producer and MMA issuer get 8 and 9)
+constexpr int kWarpTMA = 8, kWarpMMA = 9;
 constexpr int kStages = 3;
 constexpr int kChunk = 128;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kPanels = D / 64 > 0 ? D / 64 : 1;
   constexpr uint32_t kPanelBytes = kChunk * 128;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpTMA && lane == 0) {
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     for (int s = 0; s < kStages; ++s) {
@@ -119,13 +122,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&sm.aready, 8);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == kWarpMMA) tmem_alloc<512>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
-  if (warp == 0) {
+  if (warp == kWarpTMA) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       uint32_t kc = 0;
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kWarpMMA) {
     // ------------------------------ MMA issuer ------------------------------
     {  // whole warp; elected lane issues
       const uint32_t tU = tbase + kColU, tA = tbase + kColA;
@@ -199,11 +202,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       (void)pvc;
     }
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ------------------------------ softmax + epilogue ------------------------------
     // 8 warps: warp 4+qd and 8+qd share TMEM lane quadrant qd (rows r = 32 qd + lane); the
     // first ("half 0") handles chunk columns [0,64), the second [64,128).
-    const int qd = warp & 3, half = (warp - 4) >> 2;
+    const int qd = warp & 3, half = warp >> 2;
     const int r = qd * 32 + lane;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t tU = tbase + kColU + lane_off, tA = tbase + kColA + lane_off;
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_free<512>(tbase);
+  if (warp == kWarpMMA) tmem_free<512>(tbase);
 }
 
 }  // namespace
