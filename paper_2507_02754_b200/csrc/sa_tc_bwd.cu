@@ -937,48 +937,39 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
       if (!DET) {
-        // trilinear: 4 independent (row, chunk) tasks per iteration, all shared-memory loads first
-        constexpr int kU = 4;
-        for (int t0 = ft; t0 < 128 * kC8; t0 += kU * kNF) {
-          uint4 xq[kU], yk[kU], ud[kU], wv[kU];
-          uint32_t dst[kU];
-          bool ok[kU], in[kU];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int task = t0 + u * kNF;
-            in[u] = task < 128 * kC8;
-            const int r = task / kC8, tk = task % kC8;
-            const int g = r >> a.lR, kk = r & (a.R - 1);
-            const int i = q0 + g;
-            const int kpos = kbase + g + kk;
-            ok[u] = in[u] && r < a.G * a.R && i < qb && kpos >= 0;
-            int slot = sbase + g + kk;
-            if (slot >= a.ring) slot -= a.ring;
-            dst[u] = sw128_off(r, tk);
-            if (ok[u]) {
+        // trilinear: thread -> one 16-byte column chunk c8 and every ngk-th row; the q/dO chunk of
+        // the current query is kept in registers (halves the shared-memory reads per row chunk)
+        constexpr int kNgk = kNF / kC8;
+        const int c8 = ft % kC8, gk = ft / kC8;
+        int gcur = -1;
+        uint4 xq = make_uint4(0u, 0u, 0u, 0u), ud = xq;
+#pragma unroll 2
+        for (int r = gk; r < 128; r += kNgk) {
+          const int g = r >> a.lR, kk = r & (a.R - 1);
+          const int i = q0 + g;
+          const int kpos = kbase + g + kk;
+          const bool ok = r < a.G * a.R && i < qb && kpos >= 0;
+          uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
+          if (ok) {
+            if (g != gcur) {
+              gcur = g;
               const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
               const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
-              const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
-              const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
-              xq[u] = *reinterpret_cast<const uint4*>(qrow + 8 * tk);
-              yk[u] = *reinterpret_cast<const uint4*>(k2row + 8 * tk);
-              ud[u] = *reinterpret_cast<const uint4*>(dorow + 8 * tk);
-              wv[u] = *reinterpret_cast<const uint4*>(v2row + 8 * tk);
+              xq = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
+              ud = *reinterpret_cast<const uint4*>(dorow + 8 * c8);
             }
+            int slot = sbase + g + kk;
+            if (slot >= a.ring) slot -= a.ring;
+            const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
+            const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
+            const uint4 yk = *reinterpret_cast<const uint4*>(k2row + 8 * c8);
+            const uint4 wv = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
+            oa = make_uint4(hmul2_u32(xq.x, yk.x), hmul2_u32(xq.y, yk.y), hmul2_u32(xq.z, yk.z), hmul2_u32(xq.w, yk.w));
+            od = make_uint4(hmul2_u32(ud.x, wv.x), hmul2_u32(ud.y, wv.y), hmul2_u32(ud.z, wv.z), hmul2_u32(ud.w, wv.w));
           }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            if (!in[u]) continue;
-            uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
-            if (ok[u]) {
-              oa = make_uint4(hmul2_u32(xq[u].x, yk[u].x), hmul2_u32(xq[u].y, yk[u].y), hmul2_u32(xq[u].z, yk[u].z),
-                              hmul2_u32(xq[u].w, yk[u].w));
-              od = make_uint4(hmul2_u32(ud[u].x, wv[u].x), hmul2_u32(ud[u].y, wv[u].y), hmul2_u32(ud[u].z, wv[u].z),
-                              hmul2_u32(ud[u].w, wv[u].w));
-            }
-            *reinterpret_cast<uint4*>(sm.as[buf] + dst[u]) = oa;
-            *reinterpret_cast<uint4*>(sm.adp[buf] + dst[u]) = od;
-          }
+          const uint32_t dst = sw128_off(r, c8);
+          *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
+          *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
         }
       } else
       for (int task = ft; task < 128 * kTasks; task += kNF) {
