@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
 // exponent and the dK epilogue) are formed by 3 former warps from an fp16 staging ring filled
 // with cp.async one tile ahead.
 // ==========================================================================================
-constexpr int kKVThreads = 384;  // warps 0-7 softmax-gradient, 8-10 A-tile formers (8 also TMA), 11 MMA
+constexpr int kKVThreads = 416;  // warps 0-7 softmax-gradient, 8-11 A-tile formers (8 also TMA), 12 MMA
 constexpr uint32_t kKST = 0, kKdPT = 128, kKdV = 256, kKdK = 384;
 constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
 constexpr int kKVGmax = 8;    // staged queries per tile
@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     tma_prefetch(&tmV);
     mbar_init(&sm.kvload, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&sm.aready[s], 3);
+      mbar_init(&sm.aready[s], 4);
       mbar_init(&sm.afree[s], 1);
       mbar_init(&sm.sfull[s], 1);
       mbar_init(&sm.pready[s], 4);
@@ -837,13 +837,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     mbar_init(&sm.done, 1);
     fence_mbar_init();
   }
-  if (warp == 11) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 12) tmem_alloc<512>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
-  if (warp >= 8 && warp <= 10) {
+  if (warp >= 8 && warp <= 11) {
     // ------------------------------ TMA (once) + A-tile formers ------------------------------
     if (warp == 8 && lane == 0 && ntile > 0) {
       mbar_expect_tx(&sm.kvload, 2 * KVSmem<D>::kTileBytes);
@@ -852,8 +852,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         tma_load_4d(sm.vb + pn * kPanelBytes, &tmV, &sm.kvload, pn * 64, h, j0, b);
       }
     }
-    const int ft = (warp - 8) * 32 + lane;  // 0..95
-    constexpr int kNF = 96;
+    const int ft = (warp - 8) * 32 + lane;  // 0..127
+    constexpr int kNF = 128;
     // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
     auto ring_mod = [&](int kp) {  // kp mod ring for kp >= -ring (one division per call site)
       return (kp + a.ring) % a.ring;
@@ -937,37 +937,43 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
       if (!DET) {
-        // trilinear: thread -> one 16-byte column chunk c8 and every ngk-th row; the q/dO chunk of
-        // the current query is kept in registers (halves the shared-memory reads per row chunk)
-        constexpr int kNgk = kNF / kC8;
-        const int c8 = ft % kC8, gk = ft / kC8;
-        int gcur = -1;
-        uint4 xq = make_uint4(0u, 0u, 0u, 0u), ud = xq;
-#pragma unroll 2
-        for (int r = gk; r < 128; r += kNgk) {
+        // trilinear: thread -> (16-byte column chunk c8, block of kRB consecutive rows); within a
+        // block the query (and its q/dO chunk) changes at most every R rows; fully unrolled so the
+        // shared-memory loads of all rows are in flight together
+        constexpr int kRB = 128 * kC8 / kNF;  // rows per thread: 16 (D=128) or 8 (D=64)
+        const int c8 = ft % kC8, r0 = (ft / kC8) * kRB;
+        uint4 yk[kRB], wv[kRB], xq[kRB], ud[kRB];
+        bool ok[kRB];
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          const int r = r0 + u;
           const int g = r >> a.lR, kk = r & (a.R - 1);
           const int i = q0 + g;
           const int kpos = kbase + g + kk;
-          const bool ok = r < a.G * a.R && i < qb && kpos >= 0;
-          uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
-          if (ok) {
-            if (g != gcur) {
-              gcur = g;
-              const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
-              const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
-              xq = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
-              ud = *reinterpret_cast<const uint4*>(dorow + 8 * c8);
-            }
-            int slot = sbase + g + kk;
-            if (slot >= a.ring) slot -= a.ring;
+          ok[u] = r < a.G * a.R && i < qb && kpos >= 0;
+          int slot = sbase + g + kk;
+          if (slot >= a.ring) slot -= a.ring;
+          if (ok[u]) {
+            const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
+            const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
             const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
             const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
-            const uint4 yk = *reinterpret_cast<const uint4*>(k2row + 8 * c8);
-            const uint4 wv = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
-            oa = make_uint4(hmul2_u32(xq.x, yk.x), hmul2_u32(xq.y, yk.y), hmul2_u32(xq.z, yk.z), hmul2_u32(xq.w, yk.w));
-            od = make_uint4(hmul2_u32(ud.x, wv.x), hmul2_u32(ud.y, wv.y), hmul2_u32(ud.z, wv.z), hmul2_u32(ud.w, wv.w));
+            xq[u] = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
+            ud[u] = *reinterpret_cast<const uint4*>(dorow + 8 * c8);
+            yk[u] = *reinterpret_cast<const uint4*>(k2row + 8 * c8);
+            wv[u] = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
           }
-          const uint32_t dst = sw128_off(r, c8);
+        }
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
+          if (ok[u]) {
+            oa = make_uint4(hmul2_u32(xq[u].x, yk[u].x), hmul2_u32(xq[u].y, yk[u].y), hmul2_u32(xq[u].z, yk[u].z),
+                            hmul2_u32(xq[u].w, yk[u].w));
+            od = make_uint4(hmul2_u32(ud[u].x, wv[u].x), hmul2_u32(ud[u].y, wv[u].y), hmul2_u32(ud[u].z, wv[u].z),
+                            hmul2_u32(ud[u].w, wv[u].w));
+          }
+          const uint32_t dst = sw128_off(r0 + u, c8);
           *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
           *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
         }
@@ -1061,7 +1067,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       SA_TRACE_POINT(trf, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
-  } else if (warp == 11) {
+  } else if (warp == 12) {
     // ------------------------------ MMA issuer ------------------------------
     if (ntile > 0) {  // whole warp; elected lane issues
       const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
@@ -1124,12 +1130,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_wait(&sm.sfull[half], t & 1);
       tc_fence_after();
       SA_TRACE_POINT(trs, t << 16 | (52 + half) << 8);
-      uint32_t su[64], du[64];
-      tmem_ld32(tST + cb, *reinterpret_cast<uint32_t(*)[32]>(su));
-      tmem_ld32(tST + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(su + 32));
-      tmem_ld32(tdPT + cb, *reinterpret_cast<uint32_t(*)[32]>(du));
-      tmem_ld32(tdPT + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(du + 32));
-      tmem_ld_wait();
       // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
       // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
       const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
@@ -1143,22 +1143,31 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           chi = 0;
         }
       }
-      uint32_t pp[32], pd[32];
+      // two 32-column steps (register pressure); P^T / dS^T of this half go to the first 32
+      // columns of the half's own S^T / dP^T region (columns already consumed)
 #pragma unroll
-      for (int t2 = 0; t2 < 32; ++t2) {
-        const float2 r0 = sm.rinfo[buf][cb + 2 * t2], r1 = sm.rinfo[buf][cb + 2 * t2 + 1];
-        float p0 = ex2(fmaf(__uint_as_float(su[2 * t2]), sl2, -r0.x));
-        float p1 = ex2(fmaf(__uint_as_float(su[2 * t2 + 1]), sl2, -r1.x));
-        if (!all_in) {
-          p0 = (2 * t2 >= clo && 2 * t2 <= chi) ? p0 : 0.f;
-          p1 = (2 * t2 + 1 >= clo && 2 * t2 + 1 <= chi) ? p1 : 0.f;
+      for (int sub = 0; sub < 2; ++sub) {
+        uint32_t su[32], du[32];
+        tmem_ld32(tST + cb + 32 * sub, su);
+        tmem_ld32(tdPT + cb + 32 * sub, du);
+        tmem_ld_wait();
+        uint32_t pp[16], pd[16];
+#pragma unroll
+        for (int t2 = 0; t2 < 16; ++t2) {
+          const int c = 32 * sub + 2 * t2;
+          const float2 r0 = sm.rinfo[buf][cb + c], r1 = sm.rinfo[buf][cb + c + 1];
+          float p0 = ex2(fmaf(__uint_as_float(su[2 * t2]), sl2, -r0.x));
+          float p1 = ex2(fmaf(__uint_as_float(su[2 * t2 + 1]), sl2, -r1.x));
+          if (!all_in) {
+            p0 = (c >= clo && c <= chi) ? p0 : 0.f;
+            p1 = (c + 1 >= clo && c + 1 <= chi) ? p1 : 0.f;
+          }
+          pp[t2] = pack_f16x2(p0, p1);
+          pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[2 * t2]) - r0.y), p1 * (__uint_as_float(du[2 * t2 + 1]) - r1.y));
         }
-        pp[t2] = pack_f16x2(p0, p1);
-        pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[2 * t2]) - r0.y), p1 * (__uint_as_float(du[2 * t2 + 1]) - r1.y));
+        tmem_st16(tST + cb + 16 * sub, pp);
+        tmem_st16(tdPT + cb + 16 * sub, pd);
       }
-      // P^T / dS^T of this half go to the first 32 columns of the half's own S^T / dP^T region
-      tmem_st32(tST + cb, pp);
-      tmem_st32(tdPT + cb, pd);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -1219,7 +1228,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 
   __syncthreads();
   tc_fence_after();
-  if (warp == 11) tmem_free<512>(tbase);
+  if (warp == 12) tmem_free<512>(tbase);
 }
 
 }  // namespace
