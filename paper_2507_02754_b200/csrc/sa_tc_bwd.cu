@@ -937,45 +937,54 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
       if (!DET) {
-        // trilinear: thread -> (16-byte column chunk c8, block of kRB consecutive rows); within a
-        // block the query (and its q/dO chunk) changes at most every R rows; fully unrolled so the
-        // shared-memory loads of all rows are in flight together
+        // trilinear: thread -> (16-byte column chunk c8, block of kRB consecutive rows), 4 rows in
+        // flight at a time; the q/dO chunk is reloaded only when the row's query changes
         constexpr int kRB = 128 * kC8 / kNF;  // rows per thread: 16 (D=128) or 8 (D=64)
         const int c8 = ft % kC8, r0 = (ft / kC8) * kRB;
-        uint4 yk[kRB], wv[kRB], xq[kRB], ud[kRB];
-        bool ok[kRB];
+        int gcur = -1;
+        uint4 xq = make_uint4(0u, 0u, 0u, 0u), ud = xq;
 #pragma unroll
-        for (int u = 0; u < kRB; ++u) {
-          const int r = r0 + u;
-          const int g = r >> a.lR, kk = r & (a.R - 1);
-          const int i = q0 + g;
-          const int kpos = kbase + g + kk;
-          ok[u] = r < a.G * a.R && i < qb && kpos >= 0;
-          int slot = sbase + g + kk;
-          if (slot >= a.ring) slot -= a.ring;
-          if (ok[u]) {
-            const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
-            const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
-            const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
-            const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
-            xq[u] = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
-            ud[u] = *reinterpret_cast<const uint4*>(dorow + 8 * c8);
-            yk[u] = *reinterpret_cast<const uint4*>(k2row + 8 * c8);
-            wv[u] = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
-          }
-        }
+        for (int u0 = 0; u0 < kRB; u0 += 4) {
+          uint4 yk[4], wv[4];
+          bool ok[4];
 #pragma unroll
-        for (int u = 0; u < kRB; ++u) {
-          uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
-          if (ok[u]) {
-            oa = make_uint4(hmul2_u32(xq[u].x, yk[u].x), hmul2_u32(xq[u].y, yk[u].y), hmul2_u32(xq[u].z, yk[u].z),
-                            hmul2_u32(xq[u].w, yk[u].w));
-            od = make_uint4(hmul2_u32(ud[u].x, wv[u].x), hmul2_u32(ud[u].y, wv[u].y), hmul2_u32(ud[u].z, wv[u].z),
-                            hmul2_u32(ud[u].w, wv[u].w));
+          for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u0 + u;
+            const int g = r >> a.lR, kk = r & (a.R - 1);
+            const int i = q0 + g;
+            const int kpos = kbase + g + kk;
+            ok[u] = r < a.G * a.R && i < qb && kpos >= 0;
+            int slot = sbase + g + kk;
+            if (slot >= a.ring) slot -= a.ring;
+            if (ok[u]) {
+              const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
+              const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
+              yk[u] = *reinterpret_cast<const uint4*>(k2row + 8 * c8);
+              wv[u] = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
+            }
           }
-          const uint32_t dst = sw128_off(r0 + u, c8);
-          *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
-          *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int r = r0 + u0 + u;
+            const int g = r >> a.lR;
+            uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
+            if (ok[u]) {
+              if (g != gcur) {
+                gcur = g;
+                const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, q0 + g, h);
+                const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, q0 + g, h);
+                xq = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
+                ud = *reinterpret_cast<const uint4*>(dorow + 8 * c8);
+              }
+              oa = make_uint4(hmul2_u32(xq.x, yk[u].x), hmul2_u32(xq.y, yk[u].y), hmul2_u32(xq.z, yk[u].z),
+                              hmul2_u32(xq.w, yk[u].w));
+              od = make_uint4(hmul2_u32(ud.x, wv[u].x), hmul2_u32(ud.y, wv[u].y), hmul2_u32(ud.z, wv[u].z),
+                              hmul2_u32(ud.w, wv[u].w));
+            }
+            const uint32_t dst = sw128_off(r, c8);
+            *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
+            *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
+          }
         }
       } else
       for (int task = ft; task < 128 * kTasks; task += kNF) {
