@@ -45,6 +45,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescale = 8.0f;  // log2 units: rescale U only when the row max grows by > 2^8
 constexpr uint32_t kColS0 = 0, kColU0 = 128, kColA0 = 384;
+constexpr int kStgRows = 96;  // staged rows per pair (2G + 2(R+2G-1) <= 96: R in {16, 32})
 
 struct FwdArgs {
   Problem p;                // after the (K,V,w1) <-> (K',V',w2) swap: w2 = rows per query
@@ -65,6 +66,8 @@ struct Smem {
   alignas(1024) uint8_t k[kStages][kStageBytes];
   alignas(1024) uint8_t v[kStages][kStageBytes];
   float ebuf[2][128][17];
+  // staged bf16 rows of the next/current pair: q (2G), k2 (R+2G-1), v2 (R+2G-1); pitch D+8
+  alignas(16) __nv_bfloat16 stg[2][kStgRows][D + 8];
   float rm[2][128], rl[2][128];
   float gM[2][128], gL[2][128];
   uint64_t kvfull[kStages], kvempty[kStages];
@@ -95,7 +98,7 @@ __device__ __forceinline__ int chunk_width(const Item& it, int c) {
   return ((it.span - kChunk * (it.nch - 1)) + 15) & ~15;
 }
 
-template <int D>
+template <int D, bool STAGED>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -163,8 +166,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit_w(&sm.sfull[x]);
       };
+      const int tn = item / gridDim.x;
+      const bool trm = lane == 0 && tn >= 50 && tn < 52;
       mbar_wait(&sm.aready[0], gc & 1);
       mbar_wait(&sm.aready[1], gc & 1);
+      SA_TRACE_POINT(trm, tn << 16 | 10 << 8);
       mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
       tc_fence_after();
       issue_s(0, 0);
@@ -177,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int x = 0; x < 2; ++x) {
           mbar_wait(&sm.pready[x], (kc + c) & 1);
           tc_fence_after();
+          SA_TRACE_POINT(trm, tn << 16 | (11 + x) << 8 | c);
           for (int kk = 0; kk < w / 16; ++kk)
             mma_ts_w(tbase + kColU0 + 128 * x, tbase + kColS0 + 64 * x + kk * 8,
                      smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_pv, (c > 0 || kk > 0) ? 1u : 0u);
@@ -199,29 +206,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------ softmax + epilogue of tile x = warp / 4 ------------------------------
     const int x = warp >> 2, qd = warp & 3;
     const int r = qd * 32 + lane;
+    const int tid = threadIdx.x;  // 0..255
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t tS = tbase + kColS0 + 64 * x + lane_off;
     const uint32_t tU = tbase + kColU0 + 128 * x + lane_off;
     const uint32_t tA = tbase + kColA0 + 64 * x + lane_off;
     const Problem& p = a.p;
     const int g = r / a.R, kk = r % a.R;
+    const int nk2 = a.R + 2 * a.G - 1;  // k2/v2 rows of a pair
+    constexpr int kC8 = D / 8;
+    // stage the rows of pair `item` into buffer `buf` (cp.async; one commit group per call)
+    auto stage = [&](int item, int buf) {
+      if (!STAGED) return;
+      const Item it = get_item(a, item);
+      const int i0 = 2 * it.pair * a.G;
+      const int kb = p.np + i0 - a.R + 1;
+      const int nrows = 2 * a.G + 2 * nk2;
+      for (int task = tid; task < nrows * kC8; task += 256) {
+        const int row = task / kC8, c8 = task % kC8;
+        const __nv_bfloat16* src = nullptr;
+        if (row < 2 * a.G) {
+          if (i0 + row < p.N) src = a.q + p.qoff(it.b, i0 + row, it.h);
+        } else {
+          const int rr = row - 2 * a.G;
+          const int kp = kb + (rr < nk2 ? rr : rr - nk2);
+          if (kp >= 0 && kp < p.NK()) src = (rr < nk2 ? a.k2 : a.v2) + p.koff(it.b, kp, it.h);
+        }
+        if (src) cp_async16(&sm.stg[buf][row][8 * c8], src + 8 * c8);
+      }
+      cp_async_commit();
+    };
     uint32_t cc = 0, gc = 0;
+    if (blockIdx.x < a.items) stage(blockIdx.x, 0);
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
       const Item it = get_item(a, item);
+      const int buf = STAGED ? int(gc & 1) : 0;
+      if (STAGED) {
+        if (item + int(gridDim.x) < a.items) {
+          stage(item + gridDim.x, buf ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        named_bar_sync(3, 256);
+      }
       const int i0 = (2 * it.pair + x) * a.G;
       const int nq = max(0, min(a.G, p.N - i0));
       const bool row_in = r < a.G * a.R && g < nq;
       const int pos = p.np + i0 + g;
       const int kpos = pos - a.R + 1 + kk;
       const bool valid = row_in && kpos >= 0;
+      const int srow = x * a.G + g + kk;  // this row's k2/v2 staging offset
+      const __nv_bfloat16* qrow = STAGED ? &sm.stg[buf][x * a.G + g][0] : a.q + p.qoff(it.b, i0 + g, it.h);
+      const __nv_bfloat16* k2row = STAGED ? &sm.stg[buf][2 * a.G + srow][0] : a.k2 + p.koff(it.b, kpos, it.h);
+      const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2 + srow][0] : a.v2 + p.koff(it.b, kpos, it.h);
 
       // ---- A operand a_(i,k) = s log2e (q_i o k2_k)  [det: s log2e (k2_k x q_i)], fp16 -> TMEM ----
       {
         uint32_t pk[D / 2];
 #pragma unroll
         for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
-        if (valid)
-          row_operand_f16<D>(a.q + p.qoff(it.b, i0 + g, it.h), a.k2 + p.koff(it.b, kpos, it.h), a.a_scale, p.det, pk);
+        if (valid) row_operand_f16<D>(qrow, k2row, a.a_scale, p.det, pk);
         tmem_store_row<D>(tA, pk);
         tmem_st_wait();
         tc_fence_before();
@@ -309,68 +354,131 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- epilogue: merge the R rows of each query, v2 o U, normalise ----
       mbar_wait(&sm.udone[x], gc & 1);
       tc_fence_after();
-      sm.rm[x][r] = valid ? m_ref : -INFINITY;
-      sm.rl[x][r] = valid ? l : 0.f;
-      named_bar_sync(1 + x, 128);
-      if (r < nq) {
-        float M = -INFINITY;
-        for (int t = 0; t < a.R; ++t) M = fmaxf(M, sm.rm[x][r * a.R + t]);
-        float L = 0.f;
-        for (int t = 0; t < a.R; ++t) {
-          const float mt = sm.rm[x][r * a.R + t];
-          if (mt != -INFINITY) L += sm.rl[x][r * a.R + t] * ex2(mt - M);
-        }
-        sm.gM[x][r] = M;
-        sm.gL[x][r] = L;
-        a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + r] = (M + log2f(L)) * kLn2;
-      }
-      named_bar_sync(1 + x, 128);
-      const float crow = (valid && m_ref != -INFINITY) ? ex2(m_ref - sm.gM[x][g]) : 0.f;
-      const __nv_bfloat16* v2row = a.v2 + p.koff(it.b, valid ? kpos : 0, it.h);
-      float(*eb)[17] = sm.ebuf[x];
+      if (a.R == 32) {
+        // one warp == one query: group statistics and the row reduction stay in the warp
+        const bool live = valid && m_ref != -INFINITY;
+        float M = live ? m_ref : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float crow = live ? ex2(m_ref - M) : 0.f;
+        float L = live ? l * crow : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        const bool qlive = g < nq;
+        if (lane == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
+        const float invL = qlive ? 1.f / L : 0.f;
 #pragma unroll 1
-      for (int cb = 0; cb < D / 16; ++cb) {
-        uint32_t u[16];
-        tmem_ld16(tU + 16 * cb, u);
-        tmem_ld_wait();
-        float vv[16];
-        if (valid) {
-          load_bf16<16>(v2row + 16 * cb, vv);
-        } else {
+        for (int cb = 0; cb < D / 16; ++cb) {
+          uint32_t u[16];
+          tmem_ld16(tU + 16 * cb, u);
+          tmem_ld_wait();
+          float v[16];
+          if (valid) {
+            if (STAGED) {
+              const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) vv[e] = 0.f;
-        }
+              for (int t = 0; t < 2; ++t) {
+                const uint4 y = vp[t];
+                const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-        for (int e = 0; e < 16; ++e) eb[r][e] = crow * vv[e] * __uint_as_float(u[e]);
-        named_bar_sync(1 + x, 128);
-        // nq x 16 outputs, 4 lanes per output over interleaved rows, shuffle-combined
-        for (int base = 0; base < nq * 16 * 4; base += 128) {
-          const int idx = base + r;
-          const bool act = idx < nq * 16 * 4;
-          const int oo = idx >> 2, part = idx & 3;
-          const int gq = oo >> 4, d = oo & 15;
-          float y0 = 0.f, y1 = 0.f;
-          if (act) {
-            int t = part;
-            for (; t + 4 < a.R; t += 8) {
-              y0 += eb[gq * a.R + t][d];
-              y1 += eb[gq * a.R + t + 4][d];
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = bf16x2_to_f2(ys[e]);
+                  v[8 * t + 2 * e] = f.x;
+                  v[8 * t + 2 * e + 1] = f.y;
+                }
+              }
+            } else {
+              load_bf16<16>(v2row + 16 * cb, v);
             }
-            if (t < a.R) y0 += eb[gq * a.R + t][d];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] *= crow * __uint_as_float(u[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0.f;
           }
-          float y = y0 + y1;
-          y += __shfl_xor_sync(0xffffffffu, y, 1);
-          y += __shfl_xor_sync(0xffffffffu, y, 2);
-          if (act && part == 0) {
-            const float val = y / sm.gL[x][gq];
-            const int64_t off = p.qoff(it.b, i0 + gq, it.h) + 16 * cb + d;
+          // reduce-scatter the 16 columns over the 32 lanes
+#pragma unroll
+          for (int st = 16, n = 8; st >= 2; st >>= 1, n >>= 1) {
+            const bool hi = lane & st;
+#pragma unroll
+            for (int i = 0; i < n; ++i) {
+              const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+            }
+          }
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+          if ((lane & 1) == 0 && qlive) {
+            const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + col;
             if (a.out_f32)
-              reinterpret_cast<float*>(a.o)[off] = val;
+              reinterpret_cast<float*>(a.o)[off] = v[0] * invL;
             else
-              reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(val);
+              reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(v[0] * invL);
           }
         }
+      } else {
+        sm.rm[x][r] = valid ? m_ref : -INFINITY;
+        sm.rl[x][r] = valid ? l : 0.f;
         named_bar_sync(1 + x, 128);
+        if (r < nq) {
+          float M = -INFINITY;
+          for (int t = 0; t < a.R; ++t) M = fmaxf(M, sm.rm[x][r * a.R + t]);
+          float L = 0.f;
+          for (int t = 0; t < a.R; ++t) {
+            const float mt = sm.rm[x][r * a.R + t];
+            if (mt != -INFINITY) L += sm.rl[x][r * a.R + t] * ex2(mt - M);
+          }
+          sm.gM[x][r] = M;
+          sm.gL[x][r] = L;
+          a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + r] = (M + log2f(L)) * kLn2;
+        }
+        named_bar_sync(1 + x, 128);
+        const float crow = (valid && m_ref != -INFINITY) ? ex2(m_ref - sm.gM[x][g]) : 0.f;
+        float(*eb)[17] = sm.ebuf[x];
+#pragma unroll 1
+        for (int cb = 0; cb < D / 16; ++cb) {
+          uint32_t u[16];
+          tmem_ld16(tU + 16 * cb, u);
+          tmem_ld_wait();
+          float vv[16];
+          if (valid) {
+            load_bf16<16>(v2row + 16 * cb, vv);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) vv[e] = 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) eb[r][e] = crow * vv[e] * __uint_as_float(u[e]);
+          named_bar_sync(1 + x, 128);
+          // nq x 16 outputs, 4 lanes per output over interleaved rows, shuffle-combined
+          for (int base = 0; base < nq * 16 * 4; base += 128) {
+            const int idx = base + r;
+            const bool act = idx < nq * 16 * 4;
+            const int oo = idx >> 2, part = idx & 3;
+            const int gq = oo >> 4, d = oo & 15;
+            float y0 = 0.f, y1 = 0.f;
+            if (act) {
+              int t = part;
+              for (; t + 4 < a.R; t += 8) {
+                y0 += eb[gq * a.R + t][d];
+                y1 += eb[gq * a.R + t + 4][d];
+              }
+              if (t < a.R) y0 += eb[gq * a.R + t][d];
+            }
+            float y = y0 + y1;
+            y += __shfl_xor_sync(0xffffffffu, y, 1);
+            y += __shfl_xor_sync(0xffffffffu, y, 2);
+            if (act && part == 0) {
+              const float val = y / sm.gL[x][gq];
+              const int64_t off = p.qoff(it.b, i0 + gq, it.h) + 16 * cb + d;
+              if (a.out_f32)
+                reinterpret_cast<float*>(a.o)[off] = val;
+              else
+                reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(val);
+            }
+          }
+          named_bar_sync(1 + x, 128);
+        }
       }
       tc_fence_before();
       cc += it.nch;
@@ -431,17 +539,18 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
   a.items = a.npairs * p.B * p.H;
   a.a_scale = p.scale * kLog2e;
   const int grid = std::min(a.items, num_sms());
-  if (p.D == 128) {
-    size_t smem = sizeof(Smem<128>) + 1024;
-    cudaFuncSetAttribute(tc_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const bool staged = 2 * a.G + 2 * (a.R + 2 * a.G - 1) <= kStgRows;
+  auto launch = [&](auto kern, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     KernelScope ks("tc_fwd", st);
-    tc_fwd_kernel<128><<<grid, kThreads, smem, st>>>(tmK, tmV, a);
-  } else {
-    size_t smem = sizeof(Smem<64>) + 1024;
-    cudaFuncSetAttribute(tc_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    KernelScope ks("tc_fwd", st);
-    tc_fwd_kernel<64><<<grid, kThreads, smem, st>>>(tmK, tmV, a);
-  }
+    kern<<<grid, kThreads, smem, st>>>(tmK, tmV, a);
+  };
+  if (p.D == 128)
+    staged ? launch(tc_fwd_kernel<128, true>, sizeof(Smem<128>) + 1024)
+           : launch(tc_fwd_kernel<128, false>, sizeof(Smem<128>) + 1024);
+  else
+    staged ? launch(tc_fwd_kernel<64, true>, sizeof(Smem<64>) + 1024)
+           : launch(tc_fwd_kernel<64, false>, sizeof(Smem<64>) + 1024);
   return cudaGetLastError();
 }
 

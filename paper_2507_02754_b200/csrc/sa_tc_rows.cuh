@@ -25,7 +25,7 @@ __device__ __forceinline__ void row_operand_f16(const __nv_bfloat16* x, const __
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
         if (base + 8 * u < D) {
-          uint4 a = __ldg(xp + base / 8 + u), b = __ldg(yp + base / 8 + u);
+          uint4 a = xp[base / 8 + u], b = yp[base / 8 + u];  // plain loads: rows may be staged in smem
           uint32_t as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -57,7 +57,7 @@ __device__ __forceinline__ void row_operand_f16(const __nv_bfloat16* x, const __
   } else {
 #pragma unroll
     for (int t = 0; t < D / 8; ++t) {
-      uint4 a = __ldg(xp + t), b = __ldg(yp + t);
+      uint4 a = xp[t], b = yp[t];
       uint32_t as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
