@@ -81,7 +81,7 @@ __device__ __forceinline__ void load_bf16(const __nv_bfloat16* p, float (&f)[N])
   const uint4* vp = reinterpret_cast<const uint4*>(p);
 #pragma unroll
   for (int t = 0; t < N / 8; ++t) {
-    uint4 x = __ldg(vp + t);
+    uint4 x = vp[t];  // plain load: p may point into shared-memory staging
     uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
