@@ -89,7 +89,14 @@ struct QSmem {
   alignas(1024) uint8_t v[kStages][kStageBytes];
   float acc_k2[RING][D];
   float acc_v2[RING][D];
-  float eq[128][25], ek[128][25], ev[128][25];
+  union {
+    struct {
+      float eq[128][25], ek[128][25], ev[128][25];
+    } g;  // generic passes (PW <= 24)
+    struct {
+      float ek[128][33], ev[128][33];
+    } w;  // R = 32 trilinear passes (PW = 32, dq reduced in registers)
+  } eb;
   // staged rows; pitch D+8 halves so that lanes reading consecutive rows hit distinct banks
   alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D + 8];
   float slse[2][16], sdl[2][16];
@@ -173,15 +180,15 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
       for (int t = 0; t < PW; t += 3) {
         if (t + 3 <= PW && c0 + t + 3 <= D3) {
           // dq: W x k2 ; dk2: q x W     ((x cross y)_r = x_{r+1} y_{r+2} - x_{r+2} y_{r+1})
-          sm.eq[r][t + 0] = s * (wv[t + 1] * k2v[t + 2] - wv[t + 2] * k2v[t + 1]);
-          sm.eq[r][t + 1] = s * (wv[t + 2] * k2v[t + 0] - wv[t + 0] * k2v[t + 2]);
-          sm.eq[r][t + 2] = s * (wv[t + 0] * k2v[t + 1] - wv[t + 1] * k2v[t + 0]);
-          sm.ek[r][t + 0] = s * (qv[t + 1] * wv[t + 2] - qv[t + 2] * wv[t + 1]);
-          sm.ek[r][t + 1] = s * (qv[t + 2] * wv[t + 0] - qv[t + 0] * wv[t + 2]);
-          sm.ek[r][t + 2] = s * (qv[t + 0] * wv[t + 1] - qv[t + 1] * wv[t + 0]);
+          sm.eb.g.eq[r][t + 0] = s * (wv[t + 1] * k2v[t + 2] - wv[t + 2] * k2v[t + 1]);
+          sm.eb.g.eq[r][t + 1] = s * (wv[t + 2] * k2v[t + 0] - wv[t + 0] * k2v[t + 2]);
+          sm.eb.g.eq[r][t + 2] = s * (wv[t + 0] * k2v[t + 1] - wv[t + 1] * k2v[t + 0]);
+          sm.eb.g.ek[r][t + 0] = s * (qv[t + 1] * wv[t + 2] - qv[t + 2] * wv[t + 1]);
+          sm.eb.g.ek[r][t + 1] = s * (qv[t + 2] * wv[t + 0] - qv[t + 0] * wv[t + 2]);
+          sm.eb.g.ek[r][t + 2] = s * (qv[t + 0] * wv[t + 1] - qv[t + 1] * wv[t + 0]);
         } else {
 #pragma unroll
-          for (int e = t; e < t + 3 && e < PW; ++e) sm.eq[r][e] = sm.ek[r][e] = 0.f;
+          for (int e = t; e < t + 3 && e < PW; ++e) sm.eb.g.eq[r][e] = sm.eb.g.ek[r][e] = 0.f;
         }
       }
     } else if (PW == 16 && a.R == 32) {
@@ -190,7 +197,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
 #pragma unroll
       for (int e = 0; e < PW; ++e) {
         v[e & 15] = s * k2v[e] * wv[e];
-        sm.ek[r][e] = s * qv[e] * wv[e];
+        sm.eb.g.ek[r][e] = s * qv[e] * wv[e];
       }
       const int ln = r & 31;
 #pragma unroll
@@ -215,8 +222,8 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     } else {
 #pragma unroll
       for (int e = 0; e < PW; ++e) {
-        sm.eq[r][e] = s * k2v[e] * wv[e];
-        sm.ek[r][e] = s * qv[e] * wv[e];
+        sm.eb.g.eq[r][e] = s * k2v[e] * wv[e];
+        sm.eb.g.ek[r][e] = s * qv[e] * wv[e];
       }
     }
   } else {
@@ -237,7 +244,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
       for (int e = 0; e < PW; ++e) dov[e] = 0.f;
     }
 #pragma unroll
-    for (int e = 0; e < PW; ++e) sm.ev[r][e] = dov[e] * uv[e];
+    for (int e = 0; e < PW; ++e) sm.eb.g.ev[r][e] = dov[e] * uv[e];
   }
   SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 20 << 8 | c0);
   named_bar_sync(1, 256);
@@ -251,7 +258,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     const int gq = o / PW, d = o % PW;
     float x0 = 0.f, x1 = 0.f;
     if (act) {
-      const float(*rows)[25] = sm.eq + (gq << a.lR);
+      const float(*rows)[25] = sm.eb.g.eq + (gq << a.lR);
       int t = part;
       for (; t + 4 < a.R; t += 8) {
         x0 += rows[t][d];
@@ -286,8 +293,8 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
       for (int u = 0; u < 4; ++u) {  // independent loads first, then the sums
         const int gg = g0 + u;
         const int row = (gg << a.lR) + (sl - gg);
-        tk[u] = gg <= ghi ? sm.ek[row][d] : 0.f;
-        tv[u] = gg <= ghi ? sm.ev[row][d] : 0.f;
+        tk[u] = gg <= ghi ? sm.eb.g.ek[row][d] : 0.f;
+        tv[u] = gg <= ghi ? sm.eb.g.ev[row][d] : 0.f;
       }
       xk += (tk[0] + tk[1]) + (tk[2] + tk[3]);
       xv += (tv[0] + tv[1]) + (tv[2] + tv[3]);
@@ -298,6 +305,89 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     sm.acc_v2[slot][c0 + d] += xv;
   }
   SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 22 << 8 | c0);
+  named_bar_sync(1, 256);
+}
+
+// R = 32 trilinear pass over 32 columns: the warp of query g holds its 32 rows, so dq is a register
+// reduce-scatter (lane L ends with column c0+L); dk2/dv2 go through the shared-memory gather.
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                                  int c0, int half, int r, bool valid, const QRows& rw, uint32_t tW,
+                                                  uint32_t tU, int tid256) {
+  const Problem& p = a.p;
+  const float s = p.scale;
+  const int ln = r & 31;
+  if (half == 0) {
+    uint32_t u[32];
+    tmem_ld32(tW + c0, u);
+    tmem_ld_wait();
+    float k2v[32], qv[32], v[32];
+    if (valid) {
+      load_f16<32>(rw.k2 + c0, k2v);
+      load_f16<32>(rw.q + c0, qv);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) k2v[e] = qv[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const float w = __uint_as_float(u[e]);
+      v[e] = s * k2v[e] * w;
+      sm.eb.w.ek[r][e] = s * qv[e] * w;
+    }
+#pragma unroll
+    for (int st = 16, n = 16; st >= 1; st >>= 1, n >>= 1) {
+      const bool hi = ln & st;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+      }
+    }
+    const int gq = r >> 5;
+    if (gq < it.nq) {
+      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + ln;
+      if (a.out_f32)
+        reinterpret_cast<float*>(a.dq)[off] = v[0];
+      else
+        reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+    }
+  } else {
+    uint32_t u[32];
+    tmem_ld32(tU + c0, u);
+    tmem_ld_wait();
+    float dov[32];
+    if (valid) {
+      load_f16<32>(rw.dO + c0, dov);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) dov[e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) sm.eb.w.ev[r][e] = dov[e] * __uint_as_float(u[e]);
+  }
+  named_bar_sync(1, 256);
+  const int P0 = p.np + it.i0;
+  const int nsl = a.R + it.nq - 1;
+  const int sbase = (P0 - a.R + 1 + a.ring) % a.ring;
+  for (int idx = tid256; idx < nsl * 32; idx += 256) {
+    const int sl = idx >> 5, d = idx & 31;
+    const int kp = P0 - a.R + 1 + sl;
+    if (kp < 0) continue;
+    const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
+    float tk[4], tv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // G = 4 for R = 32
+      const int gg = glo + u;
+      const int row = (gg << 5) + (sl - gg);
+      tk[u] = gg <= ghi ? sm.eb.w.ek[row][d] : 0.f;
+      tv[u] = gg <= ghi ? sm.eb.w.ev[row][d] : 0.f;
+    }
+    int slot = sbase + sl;
+    if (slot >= a.ring) slot -= a.ring;
+    sm.acc_k2[slot][c0 + d] += (tk[0] + tk[1]) + (tk[2] + tk[3]);
+    sm.acc_v2[slot][c0 + d] += (tv[0] + tv[1]) + (tv[2] + tv[3]);
+  }
   named_bar_sync(1, 256);
 }
 
@@ -664,6 +754,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
           q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
         if constexpr (D % 24 != 0)
           q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256);
+      } else if (a.R == 32) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 32)
+          q_epilogue_pass32<D, RING, STAGED>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
       } else {
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 16)
