@@ -25,8 +25,10 @@
  *   Input dtype (q,k,v,k2,v2,dO): bf16, or fp32 with SA_IN_F32.
  *   Output dtype (o, dq, dk, dv, dk2, dv2): fp32 if SA_OUT_F32 or SA_IN_F32, else bf16.
  *   The backward reads o in the output dtype.
- * OWNERSHIP.  The library never allocates device memory; the backward workspace is caller-provided
- *   (size from simplicial_attn_bwd_workspace_bytes).  Outputs must not alias inputs.
+ * OWNERSHIP.  The library allocates no device memory except the stream-ordered forward scratch of
+ *   simplicial_attn_fwd / _prefixed (cudaMallocAsync/cudaFreeAsync on `stream`); simplicial_attn_fwd_ws
+ *   and the backward take caller-provided workspaces (sizes from the *_workspace_bytes queries).
+ *   Outputs must not alias inputs.
  * EXECUTION.  Asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy default
  *   stream).  Results are valid after the caller synchronises.  Deterministic: no atomics on the
  *   data path, identical bits run to run.  Stateless and thread-safe (only cached driver entry
@@ -77,6 +79,18 @@ sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void*
                                        const void* v2, void* o, float* lse, int64_t B, int64_t H,
                                        int64_t N, int64_t D, int64_t w1, int64_t w2,
                                        int64_t n_prefix, uint32_t flags, void* stream);
+
+/* Forward with a caller-provided device workspace (the bf16 tensor-core path keeps fp16 copies of
+ * the long-window K and V there; the plain simplicial_attn_fwd takes that scratch stream-ordered
+ * from cudaMallocAsync instead).  Size from simplicial_attn_fwd_workspace_bytes; 0 is valid for
+ * paths that need none.  Otherwise identical to simplicial_attn_fwd_prefixed. */
+size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                           int64_t w2, int64_t n_prefix, uint32_t flags);
+sa_status simplicial_attn_fwd_ws(const void* q, const void* k, const void* v, const void* k2,
+                                 const void* v2, void* o, float* lse, void* workspace,
+                                 size_t workspace_bytes, int64_t B, int64_t H, int64_t N, int64_t D,
+                                 int64_t w1, int64_t w2, int64_t n_prefix, uint32_t flags,
+                                 void* stream);
 
 /* Bytes of device workspace the backward needs (delta_i [B,H,N] fp32, fp16 copies of the
  * key-side operands, band partials).  The _prefixed form sizes it for n_prefix halo rows. */

@@ -23,7 +23,8 @@ SA_PATH_TCGEN05 = 2
 _STATUS = {0: "SA_OK", 1: "SA_ERR_INVALID_ARG", 2: "SA_ERR_UNSUPPORTED", 3: "SA_ERR_WORKSPACE",
            4: "SA_ERR_CUDA"}
 EXPORTS = (
-    "simplicial_attn_fwd", "simplicial_attn_fwd_prefixed", "simplicial_attn_bwd_workspace_bytes",
+    "simplicial_attn_fwd", "simplicial_attn_fwd_prefixed", "simplicial_attn_fwd_workspace_bytes",
+    "simplicial_attn_fwd_ws", "simplicial_attn_bwd_workspace_bytes",
     "simplicial_attn_bwd_workspace_bytes_prefixed",
     "simplicial_attn_bwd", "simplicial_attn_bwd_prefixed", "simplicial_attn_host_step_scratch_bytes",
     "simplicial_attn_host_step", "simplicial_attn_fwd_path", "simplicial_attn_bwd_path",
@@ -51,6 +52,8 @@ def load_library(build: bool = True):
     sig = {
         "simplicial_attn_fwd": ([P] * 7 + [I] * 6 + [U, P], ctypes.c_int),
         "simplicial_attn_fwd_prefixed": ([P] * 7 + [I] * 7 + [U, P], ctypes.c_int),
+        "simplicial_attn_fwd_workspace_bytes": ([I] * 7 + [U], S),
+        "simplicial_attn_fwd_ws": ([P] * 8 + [S] + [I] * 7 + [U, P], ctypes.c_int),
         "simplicial_attn_bwd_workspace_bytes": ([I] * 6 + [U], S),
         "simplicial_attn_bwd_workspace_bytes_prefixed": ([I] * 7 + [U], S),
         "simplicial_attn_bwd": ([P] * 14 + [S] + [I] * 6 + [U, P], ctypes.c_int),
@@ -121,6 +124,20 @@ def _check_inputs(q, keys, n_prefix):
     return B, N, H, D
 
 
+_ws_cache: dict = {}
+
+
+def _workspace(device, nbytes: int, kind: str = "fwd") -> torch.Tensor:
+    """Per-(device, stream) scratch reused across calls; calls on one stream are ordered, so reuse
+    is safe."""
+    key = (kind, device.type, device.index, torch.cuda.current_stream(device).cuda_stream)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < max(nbytes, 1):
+        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
 def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool = False,
             n_prefix: int = 0, force_simt: bool = False):
     """o, lse = 2-simplicial attention forward (simplicial_attn_fwd_prefixed)."""
@@ -129,8 +146,10 @@ def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool 
     flags = _flags(q.dtype, det, out_f32, force_simt)
     o = torch.empty((B, N, H, D), dtype=_out_dtype(flags), device=q.device)
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
-    st = L.simplicial_attn_fwd_prefixed(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
-                                        B, H, N, D, w1, w2, n_prefix, flags, _stream(q.device))
+    wsb = int(L.simplicial_attn_fwd_workspace_bytes(B, H, N, D, w1, w2, n_prefix, flags))
+    ws = _workspace(q.device, wsb)
+    st = L.simplicial_attn_fwd_ws(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
+                                  _ptr(ws), ws.numel(), B, H, N, D, w1, w2, n_prefix, flags, _stream(q.device))
     _check(st, "simplicial_attn_fwd")
     return o, lse
 
@@ -148,7 +167,7 @@ def backward(q, k, v, k2, v2, o, lse, dO, w1: int, w2: int, det: bool = False, o
     dk, dv, dk2, dv2 = (torch.empty_like(k, dtype=od) for _ in range(4))
     wsb = int(L.simplicial_attn_bwd_workspace_bytes_prefixed(B, H, N, D, w1, w2, n_prefix, flags))
     if workspace is None or workspace.numel() < wsb:
-        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=q.device)
+        workspace = _workspace(q.device, wsb, "bwd")
     st = L.simplicial_attn_bwd_prefixed(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
                                         _ptr(dO), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dk2), _ptr(dv2),
                                         _ptr(workspace), workspace.numel(), B, H, N, D, w1, w2, n_prefix,

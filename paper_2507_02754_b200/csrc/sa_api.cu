@@ -28,12 +28,24 @@ static std::atomic<int> g_prof_on{0};
 static std::mutex g_prof_mu;
 static std::vector<ProfRec> g_prof;
 
+static std::vector<cudaEvent_t> g_event_pool;  // recycled by simplicial_attn_profile_read
+static cudaEvent_t pooled_event() {
+  cudaEvent_t e = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (!g_event_pool.empty()) {
+      e = g_event_pool.back();
+      g_event_pool.pop_back();
+    }
+  }
+  if (!e) cudaEventCreate(&e);
+  return e;
+}
+
 KernelScope::KernelScope(const char* name, cudaStream_t s) : slot(-1), st(s) {
   note_launch(1);
   if (!g_prof_on.load(std::memory_order_relaxed)) return;
-  ProfRec r{name, nullptr, nullptr};
-  cudaEventCreate(&r.a);
-  cudaEventCreate(&r.b);
+  ProfRec r{name, pooled_event(), pooled_event()};
   cudaEventRecord(r.a, st);
   std::lock_guard<std::mutex> g(g_prof_mu);
   slot = int(g_prof.size());
@@ -58,8 +70,11 @@ cudaError_t simt_backward(const Problem& p, bool in_f32, bool out_f32, const voi
 
 // tcgen05 path (sa_tc_fwd.cu / sa_tc_bwd.cu)
 bool tc_fwd_supported(const Problem& p);
+size_t tc_fwd_workspace_bytes(const Problem& p);
 cudaError_t tc_forward(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
                        const void* k2, const void* v2, void* o, float* lse, cudaStream_t st);
+cudaError_t tc_forward_ws(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
+                          const void* k2, const void* v2, void* o, float* lse, void* ws, cudaStream_t st);
 bool tc_bwd_supported(const Problem& p);
 size_t tc_bwd_workspace_bytes(const Problem& p);
 cudaError_t tc_backward(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
@@ -127,6 +142,31 @@ sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void*
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   cudaGetLastError();  // clear stale errors so a failure below is ours
   if (use_tc_fwd(p, flags)) return cuda_status(tc_forward(p, out_f32, q, k, v, k2, v2, o, lse, st));
+  return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
+}
+
+size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                           int64_t n_prefix, uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p) != SA_OK) return 0;
+  return use_tc_fwd(p, flags) ? tc_fwd_workspace_bytes(p) : 0;
+}
+
+sa_status simplicial_attn_fwd_ws(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                                 void* o, float* lse, void* workspace, size_t workspace_bytes, int64_t B, int64_t H,
+                                 int64_t N, int64_t D, int64_t w1, int64_t w2, int64_t n_prefix, uint32_t flags,
+                                 void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse) return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p);
+  if (s != SA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  cudaGetLastError();
+  if (use_tc_fwd(p, flags)) {
+    if (!workspace || workspace_bytes < tc_fwd_workspace_bytes(p)) return SA_ERR_WORKSPACE;
+    return cuda_status(tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, workspace, st));
+  }
   return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
 }
 
@@ -261,7 +301,15 @@ int simplicial_attn_bwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t
 
 uint64_t simplicial_attn_launch_count(void) { return g_launches.load(); }
 
-void simplicial_attn_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+void simplicial_attn_profile_enable(int on) {
+  if (on) {  // pre-create events so that enabling costs nothing inside a timed region
+    std::vector<cudaEvent_t> fresh(256);
+    for (auto& e : fresh) cudaEventCreateWithFlags(&e, cudaEventDefault);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_event_pool.insert(g_event_pool.end(), fresh.begin(), fresh.end());
+  }
+  g_prof_on.store(on ? 1 : 0);
+}
 
 int simplicial_attn_profile_read(char* names32, double* total_ms, int64_t* counts, int max_kernels) {
   std::vector<ProfRec> recs;
@@ -276,8 +324,11 @@ int simplicial_attn_profile_read(char* names32, double* total_ms, int64_t* count
     cudaEventSynchronize(r.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
+    {
+      std::lock_guard<std::mutex> g(g_prof_mu);
+      g_event_pool.push_back(r.a);
+      g_event_pool.push_back(r.b);
+    }
     size_t k = 0;
     while (k < names.size() && names[k] != r.name) ++k;
     if (k == names.size()) { names.push_back(r.name); tot.push_back(0); cnt.push_back(0); }

@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
             tmem_ld16(tdP + cb, du);
           }
           tmem_ld_wait();
+          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 60 << 8 | c);
           const int jc0 = it.jbeg + c * kQChunk + cb;
           int lo_c = jlo - jc0, hi_c = min(pos - jc0, nw - 1);
           if (!valid) {
@@ -730,6 +731,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
               pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
             }
           }
+          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 61 << 8 | c);
           if (nw == 32) {
             tmem_st16(tS + cb, pp);
             tmem_st16(tdP + cb, pd);
@@ -738,6 +740,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
             tmem_st8(tdP + cb, pd);
           }
           tmem_st_wait();
+          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 62 << 8 | c);
         }
         tc_fence_before();
         __syncwarp();
