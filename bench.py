@@ -153,9 +153,13 @@ def oracle_sample(c, seed, L):
 def calibrate_oracle_rows(c, target_s):
     import oracle
     oracle.build()
-    L0 = 32
+    # two-point calibration: the halo makes the cost affine in L (t = a + b L)
+    L0, L1 = 32, 160
     t0, _ = oracle_sample(c, 0, L0)
-    L = int(min(c["N"] - 1, max(L0, L0 * target_s / max(t0, 1e-3))))
+    t1, _ = oracle_sample(c, 0, L1)
+    b = max((t1 - t0) / (L1 - L0), 1e-6)
+    a = max(t0 - b * L0, 0.0)
+    L = int(min(c["N"] - 1, max(L0, (target_s - a) / b)))
     return L
 
 
@@ -198,12 +202,12 @@ def run_reference(args, c):
     print(json.dumps(line), flush=True)
 
 
-def config_block(c, n):
+def config_block(c, n, mode="bh"):
     return {"workload": f"{c['name']}: B={c['B']} H={c['H']} N={c['N']} D={c['D']} w1={c['w1']} w2={c['w2']} "
                         f"{'det' if c['det'] else 'trilinear'} {'fwd+bwd' if c['bwd'] else 'fwd'} per GPU",
             "B": c["B"], "H": c["H"], "N": c["N"], "D": c["D"], "w1": c["w1"], "w2": c["w2"],
             "variant": "det" if c["det"] else "trilinear", "global_batch_heads": c["B"] * c["H"] * n,
-            "seq_len": c["N"], "parallelism": f"bh-sharded x{n}",
+            "seq_len": c["N"], "parallelism": f"{mode}-sharded x{n}",
             "l2": "inputs larger than L2 (no flush): %.0f MB of inputs per step" % (
                 6 * c["B"] * c["N"] * c["H"] * c["D"] * 2 / 1e6),
             "flop_basis": "paper formula: fwd 6*NW*D + bwd 21*NW*D, NW = B*H*N*w1*w2"}
@@ -220,6 +224,9 @@ def main():
     ap.add_argument("--out-f32", action="store_true", help="write o/grads in fp32 (parity runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="bh", choices=["bh", "seq"],
+                    help="bh: each rank runs its own B*H shard (weak scaling, no collective); seq: the "
+                         "sequence is split across ranks (N per rank fixed) with the NCCL halo exchange")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config], name=args.config)
 
@@ -251,6 +258,14 @@ def main():
 
     def step():
         nonlocal o, lse, ws
+        if args.mode == "seq" and world > 1:
+            from paper_2507_02754_b200 import parallel
+            o, lse, ext = parallel.seq_forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, sa.forward,
+                                               det=det, out_f32=args.out_f32)
+            if c["bwd"]:
+                parallel.seq_backward(t["q"], ext, o, lse, t["dO"], w1, w2, sa.backward, det=det,
+                                      out_f32=args.out_f32)
+            return
         o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, det=det, out_f32=args.out_f32)
         if c["bwd"]:
             sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2, det=det,
@@ -387,7 +402,7 @@ def main():
             "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "compute": "bf16 inputs; fp16 MMA operands, fp32 accumulate (tcgen05) / fp32 (SIMT)",
             "data": "synthetic",
-            "config": config_block(c, world),
+            "config": config_block(c, world, args.mode),
             "mma_basis_tflops": mma_tflops,
             "pct_bf16_peak_mma_basis": 100.0 * mma_tflops / (peak_sust * world),
             "pct_bf16_peak_paper_basis": 100.0 * value / (peak_sust * world),

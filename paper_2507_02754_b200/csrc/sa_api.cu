@@ -362,13 +362,11 @@ const char* simplicial_attn_version(void) { return "libsimplicial sm_100a " __DA
 // Trace builds only: copy the (tag, clock) pairs recorded since the last call and reset.
 int simplicial_attn_debug_trace(unsigned long long* host, int max_pairs) {
   cudaDeviceSynchronize();
-  unsigned int n = 0;
-  cudaMemcpyFromSymbol(&n, sa::g_trace_n, sizeof(n));
-  n = n / 2 < unsigned(max_pairs) ? n / 2 : unsigned(max_pairs);
+  const int n = max_pairs < 4096 ? max_pairs : 4096;
   cudaMemcpyFromSymbol(host, sa::g_trace, sizeof(unsigned long long) * 2 * n);
-  unsigned int z = 0;
-  cudaMemcpyToSymbol(sa::g_trace_n, &z, sizeof(z));
-  return int(n);
+  static unsigned long long zeros[8192];
+  cudaMemcpyToSymbol(sa::g_trace, zeros, sizeof(zeros));
+  return n;
 }
 #endif
 

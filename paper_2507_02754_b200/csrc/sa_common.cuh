@@ -57,23 +57,28 @@ struct KernelScope {
 }  // namespace sa
 
 // ---- optional phase tracing (tools/trace_build.py builds a separate library with -DSA_TRACE) ----
+// SA_TRACE_AT(cond, region, n, tag): when cond holds in CTA 0, store (tag, clock64) at
+// g_trace[region*1024 + 2n] and bump the caller's register counter n (no atomics, ~no overhead).
 #ifdef SA_TRACE
 namespace sa {
 extern __device__ unsigned long long g_trace[8192];
 extern __device__ unsigned int g_trace_n;
 }
-// record (tag, clock) from the calling thread of CTA 0 when `cond` holds
-#define SA_TRACE_POINT(cond, tag)                                                                    \
-  do {                                                                                              \
-    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0) {                                             \
-      unsigned int _n = atomicAdd(&::sa::g_trace_n, 2u);                                            \
-      if (_n + 1 < 8192) {                                                                          \
-        ::sa::g_trace[_n] = (unsigned long long)(tag);                                              \
-        ::sa::g_trace[_n + 1] = (unsigned long long)clock64();                                      \
-      }                                                                                             \
-    }                                                                                               \
+#define SA_TRACE_AT(cond, region, n, tag)                                                   \
+  do {                                                                                     \
+    if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && (n) < 511) {                       \
+      ::sa::g_trace[(region) * 1024 + 2 * (n)] = (unsigned long long)(tag);               \
+      ::sa::g_trace[(region) * 1024 + 2 * (n) + 1] = (unsigned long long)clock64();       \
+      ++(n);                                                                               \
+    }                                                                                      \
+  } while (0)
+#define SA_TRACE_POINT(cond, tag) \
+  do {                            \
   } while (0)
 #else
+#define SA_TRACE_AT(cond, region, n, tag) \
+  do {                                    \
+  } while (0)
 #define SA_TRACE_POINT(cond, tag) \
   do {                            \
   } while (0)

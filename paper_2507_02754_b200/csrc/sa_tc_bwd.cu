@@ -246,9 +246,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
 #pragma unroll
     for (int e = 0; e < PW; ++e) sm.eb.g.ev[r][e] = dov[e] * uv[e];
   }
-  SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 20 << 8 | c0);
   named_bar_sync(1, 256);
-  SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 21 << 8 | c0);
   // dq: sum over the R rows of each query; 4 lanes per output, rows interleaved, shuffle-combined
   const bool dq_done = !DET && PW == 16 && a.R == 32;
   for (int base = 0; !dq_done && base < it.nq * PW * 4; base += 256) {
@@ -304,7 +302,6 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     sm.acc_k2[slot][c0 + d] += xk;
     sm.acc_v2[slot][c0 + d] += xv;
   }
-  SA_TRACE_POINT(threadIdx.x == 0 && it.grp == 100, 22 << 8 | c0);
   named_bar_sync(1, 256);
 }
 
@@ -457,12 +454,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const uint32_t tAS = tbase + kQAS, tAdP = tbase + kQAdP;
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
       uint32_t kc = 0, gc = 0;
+      int trn = 0;
       for (int item = it_begin; item < it_end; ++item) {
         QItem it = q_item(a, item);
-        const bool tr = item - it_begin >= 100 && item - it_begin < 103;
+        const bool trm = lane == 0 && item - it_begin >= 100 && item - it_begin < 102;
         mbar_wait(&sm.aready, gc & 1);
+        SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | 10 << 8);
         tc_fence_after();
-        SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 10 << 8);
         // Issue order per chunk c and half hh (hh = column halves [32hh, 32hh+32) of a 64-row chunk):
         //   S_hh(0), dP_hh(0) ... then for each c: [P_hh(c) ready] W_hh(c), U_hh(c); S_hh(c+1), dP_hh(c+1)
         // so half a's next S overlaps half b's softmax (the tensor pipe is in-order, so S_hh(c+1)
@@ -494,11 +492,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
           const int s = (kc + c) % kStages;
           const int w = q_width(it, c);
           const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
-          SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 11 << 8 | c);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             mbar_wait(&sm.pready[hh], (kc + c) & 1);
             tc_fence_after();
+            SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | (11 + hh) << 8 | c);
             const int nwh = min(32, w - 32 * hh);
             for (int k2i = 0; k2i < nwh / 16; ++k2i) {
               const uint32_t acc = (c > 0 || hh > 0 || k2i > 0) ? 1u : 0u;
@@ -515,7 +513,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
               issue_s(c + 1, hh);
             }
           }
-          SA_TRACE_POINT(tr && lane == 0, (item - it_begin) << 16 | 12 << 8 | c);
           mma_commit_w(&sm.kvempty[s]);
         }
         mma_commit_w(&sm.udone);
@@ -567,12 +564,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
     };
     uint32_t kc = 0, gc = 0;
     int PS = 0, flush_lo = 0;
+    int trn = 0;
     if (it_begin < it_end) stage(it_begin, 0);
     for (int item = it_begin; item < it_end; ++item) {
       QItem it = q_item(a, item);
+      const bool tr = (threadIdx.x & 127) == 0 && item - it_begin >= 100 && item - it_begin < 102;
+      const int treg = 1 + half;
+      SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 1 << 8);
       const int buf = STAGED ? int(gc & 1) : 0;
-      const bool tr = threadIdx.x == 0 && item - it_begin >= 100 && item - it_begin < 103;
-      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 1 << 8);
       if (STAGED) {
         if (item + 1 < it_end) {
           stage(item + 1, buf ^ 1);
@@ -682,7 +681,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.aready);
-        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 2 << 8);
+        SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 2 << 8);
       }
       // ---- chunks: P = exp(S - lse), dS = P (dP - delta), this half's 32 columns ----
       const int jlo = max(0, pos - p.w1 + 1);
@@ -692,7 +691,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const int nw = max(0, min(32, w - cb));
         mbar_wait(&sm.sfull[half], (kc + c) & 1);
         tc_fence_after();
-        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 3 << 8 | c);
+        SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 3 << 8 | c);
         if (nw > 0) {
           uint32_t su[32], du[32];
           if (nw == 32) {
@@ -703,7 +702,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
             tmem_ld16(tdP + cb, du);
           }
           tmem_ld_wait();
-          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 60 << 8 | c);
           const int jc0 = it.jbeg + c * kQChunk + cb;
           int lo_c = jlo - jc0, hi_c = min(pos - jc0, nw - 1);
           if (!valid) {
@@ -731,7 +729,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
               pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
             }
           }
-          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 61 << 8 | c);
           if (nw == 32) {
             tmem_st16(tS + cb, pp);
             tmem_st16(tdP + cb, pd);
@@ -740,17 +737,16 @@ __global__ void __launch_bounds__(kQThreads, 1)
             tmem_st8(tdP + cb, pd);
           }
           tmem_st_wait();
-          SA_TRACE_POINT(tr, (item - it_begin) << 16 | 62 << 8 | c);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pready[half]);
-        SA_TRACE_POINT(tr, (item - it_begin) << 16 | 4 << 8 | c);
+        SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 4 << 8 | c);
       }
       // ---- epilogue ----
       mbar_wait(&sm.udone, gc & 1);
       tc_fence_after();
-      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 5 << 8);
+      SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 5 << 8);
       if (DET) {
 #pragma unroll 1
         for (int c0 = 0; c0 + 24 <= D; c0 += 24)
@@ -767,7 +763,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
           q_epilogue_pass<D, RING, STAGED, 16, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
       }
       tc_fence_before();
-      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 6 << 8);
       // ---- flush ring rows that no later tile of this sub-range touches ----
       const int PE = P0 + it.nq;
       const int flush_hi = last_in_sub ? PE - 1 : P0 + a.G - a.R;  // inclusive
@@ -806,7 +801,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       }
       flush_lo = flush_hi + 1;
       named_bar_sync(1, 256);
-      SA_TRACE_POINT(tr, (item - it_begin) << 16 | 7 << 8);
+      SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 7 << 8);
       kc += it.nch;
       ++gc;
     }
@@ -1006,10 +1001,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         named_bar_sync(2, kNF);
       }
-      const bool trf = ft == 0 && t >= 50 && t < 53;
-      SA_TRACE_POINT(trf, t << 16 | 30 << 8);
       mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
-      SA_TRACE_POINT(trf, t << 16 | 31 << 8);
       // row info: (lse * log2e, delta), +inf marks rows outside the problem
       const int kbase = p.np + q0 - a.R + 1;  // key row of tile row 0
       const int sbase = STAGED ? ring_mod(kbase) : 0;
@@ -1170,7 +1162,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.aready[buf]);
-      SA_TRACE_POINT(trf, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
   } else if (warp == 12) {
@@ -1185,8 +1176,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int buf = t & 1;
         mbar_wait(&sm.aready[buf], (t >> 1) & 1);
         tc_fence_after();
-        const bool trm = lane == 0 && t >= 50 && t < 53;
-        SA_TRACE_POINT(trm, t << 16 | 40 << 8);
         const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -1213,7 +1202,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             mma_ts_w(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
           }
         }
-        SA_TRACE_POINT(trm, t << 16 | 41 << 8);
         mma_commit_w(&sm.afree[buf]);
       }
       mma_commit_w(&sm.done);
@@ -1231,11 +1219,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
       const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
-      const bool trs = threadIdx.x == 128 * half && t >= 50 && t < 53;
-      SA_TRACE_POINT(trs, t << 16 | (50 + half) << 8);
       mbar_wait(&sm.sfull[half], t & 1);
       tc_fence_after();
-      SA_TRACE_POINT(trs, t << 16 | (52 + half) << 8);
       // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
       // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
       const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
@@ -1278,7 +1263,6 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.pready[half]);
-      SA_TRACE_POINT(trs, t << 16 | (54 + half) << 8);
     }
     // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns; dK carries the scale s
     if (ntile > 0) {

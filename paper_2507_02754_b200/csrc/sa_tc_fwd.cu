@@ -152,8 +152,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------ MMA issuer (whole warp, elected lane issues) ------------------------------
     const uint32_t idesc_pv = idesc_f16(128, D, 0, 1);
     uint32_t kc = 0, gc = 0;
+    int trn = 0;
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
       const Item it = get_item(a, item);
+      const int tn = item / gridDim.x;
+      const bool trm = lane == 0 && tn >= 50 && tn < 52;
       auto issue_s = [&](int c, int x) {
         const int s = (kc + c) % kStages;
         const uint32_t idesc_s = idesc_f16(128, chunk_width(it, c), 0, 0);
@@ -166,11 +169,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit_w(&sm.sfull[x]);
       };
-      const int tn = item / gridDim.x;
-      const bool trm = lane == 0 && tn >= 50 && tn < 52;
       mbar_wait(&sm.aready[0], gc & 1);
       mbar_wait(&sm.aready[1], gc & 1);
-      SA_TRACE_POINT(trm, tn << 16 | 10 << 8);
+      SA_TRACE_AT(trm, 0, trn, tn << 16 | 10 << 8);
       mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
       tc_fence_after();
       issue_s(0, 0);
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int x = 0; x < 2; ++x) {
           mbar_wait(&sm.pready[x], (kc + c) & 1);
           tc_fence_after();
-          SA_TRACE_POINT(trm, tn << 16 | (11 + x) << 8 | c);
+          SA_TRACE_AT(trm, 0, trn, tn << 16 | (11 + x) << 8 | c);
           for (int kk = 0; kk < w / 16; ++kk)
             mma_ts_w(tbase + kColU0 + 128 * x, tbase + kColS0 + 64 * x + kk * 8,
                      smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_pv, (c > 0 || kk > 0) ? 1u : 0u);
@@ -237,9 +238,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       cp_async_commit();
     };
     uint32_t cc = 0, gc = 0;
+    int trn = 0;
     if (blockIdx.x < a.items) stage(blockIdx.x, 0);
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
       const Item it = get_item(a, item);
+      const int tn = item / gridDim.x;
+      const bool trs = r == 0 && tn >= 50 && tn < 52;
+      SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 20 << 8);
       const int buf = STAGED ? int(gc & 1) : 0;
       if (STAGED) {
         if (item + int(gridDim.x) < a.items) {
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.aready[x]);
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 21 << 8);
       }
 
       // ---- chunks: per-row online softmax (conditional rescaling) ----
@@ -281,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int w = chunk_width(it, c);
         mbar_wait(&sm.sfull[x], (cc + c) & 1);
         tc_fence_after();
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 22 << 8 | c);
         float sv[64];
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(sv);
@@ -290,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (w == 48) tmem_ld16(tS + 32, su + 32);
           tmem_ld_wait();
         }
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 23 << 8 | c);
         const int jc0 = it.jbeg + c * kChunk;
         int lo_c = jlo - jc0, hi_c = min(pos - jc0, w - 1);
         if (!valid) {
@@ -341,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[t] = pack_f16x2(p0, p1);
         }
         l += ls;  // columns >= w were masked to -inf above (need_mask holds whenever w < 64)
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 24 << 8 | c);
         if (w == 64) tmem_st32(tS, pk);
         if (w == 32 || w == 48) tmem_st16(tS, pk);
         if (w == 48) tmem_st8(tS + 16, pk + 16);
@@ -349,11 +358,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pready[x]);
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 25 << 8 | c);
       }
 
       // ---- epilogue: merge the R rows of each query, v2 o U, normalise ----
       mbar_wait(&sm.udone[x], gc & 1);
       tc_fence_after();
+      SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 26 << 8);
       if (a.R == 32) {
         // one warp == one query: group statistics and the row reduction stay in the warp
         const bool live = valid && m_ref != -INFINITY;
@@ -481,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
+      SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 27 << 8);
       cc += it.nch;
       ++gc;
     }

@@ -159,3 +159,28 @@ def test_baseline_config_sampled(cfg):
                 lo, hi, r = ref[n]
                 if hi > lo:
                     assert maxabs(got[n][b, lo:hi, h], r) <= TOL_BF16, (n, b, h, a)
+
+
+@pytest.mark.parametrize("det", [False, True])
+def test_sequence_sharded_cuda_simulated(det):
+    """The sequence-sharded composition (parallel.py) with the CUDA kernels, ranks simulated in one
+    process: each shard runs the prefixed entry points with a max(w1,w2)-1 row halo, halo-row
+    gradients are added back to their owner; the result matches the unsharded CUDA run."""
+    B, N, H, D, w1, w2, world = 1, 512, 2, 128, 96, 32, 4
+    inp = make_inputs(B, N, H, D, seed=21, dtype="bf16")
+    full = run_cuda(inp, w1, w2, det)
+    L, nh = N // world, max(w1, w2) - 1
+    key_acc = {n: torch.zeros_like(full[n]) for n in ("dk", "dv", "dk2", "dv2")}
+    for r in range(world):
+        lo = r * L
+        npf = min(nh, lo)
+        sl_q, sl_k = slice(lo, lo + L), slice(lo - npf, lo + L)
+        shard = {n: (x[:, sl_k] if n in ("k", "v", "k2", "v2") else x[:, sl_q]).contiguous() for n, x in inp.items()}
+        got = run_cuda(shard, w1, w2, det, n_prefix=npf)
+        assert maxabs(got["o"], full["o"][:, sl_q]) <= 1e-5
+        assert maxabs(got["lse"], full["lse"][:, :, sl_q]) <= 1e-5
+        assert maxabs(got["dq"], full["dq"][:, sl_q]) <= 1e-4
+        for n in key_acc:
+            key_acc[n][:, sl_k] += got[n]
+    for n in key_acc:
+        assert maxabs(key_acc[n], full[n]) <= 1e-4, n

@@ -22,11 +22,11 @@ for rep in range(2):
     o, lse = binding.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], c["w1"], c["w2"], det=c["det"])
     torch.cuda.synchronize()
     n = L.simplicial_attn_debug_trace(buf, 4096)
-    fwd = [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
+    fwd = [(buf[2 * i], buf[2 * i + 1]) for i in range(n) if buf[2 * i + 1]]
     binding.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], c["w1"], c["w2"], det=c["det"])
     torch.cuda.synchronize()
     n = L.simplicial_attn_debug_trace(buf, 4096)
-    bwd = [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
+    bwd = [(buf[2 * i], buf[2 * i + 1]) for i in range(n) if buf[2 * i + 1]]
 for name, ev in (("fwd", fwd), ("bwd", bwd)):
     if not ev:
         continue
