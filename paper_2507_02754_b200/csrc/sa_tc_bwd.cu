@@ -989,9 +989,12 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       cp_async_commit();
     };
     if (STAGED && ntile > 0) stage(0);
+    int trn = 0;
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
       const int q0 = qa + t * a.G;
+      const bool trf = ft == 0 && t >= 50 && t < 53;
+      SA_TRACE_AT(trf, 3, trn, t << 16 | 30 << 8);
       if (STAGED) {
         if (t + 1 < ntile) {
           stage(t + 1);
@@ -1002,6 +1005,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         named_bar_sync(2, kNF);
       }
       mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
+      SA_TRACE_AT(trf, 3, trn, t << 16 | 31 << 8);
       // row info: (lse * log2e, delta), +inf marks rows outside the problem
       const int kbase = p.np + q0 - a.R + 1;  // key row of tile row 0
       const int sbase = STAGED ? ring_mod(kbase) : 0;
@@ -1025,7 +1029,55 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kWS = DET ? 24 : 8;       // A_S task width (elements)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
-      if (!DET) {
+      if (!DET && STAGED && a.G <= 4) {
+        // trilinear, key-row major: thread -> (column chunk c8, key rows kp_rel = grp, grp+ngrp, ...).
+        // Each staged k2/v2 chunk is read once and multiplied into the (up to G) tile rows
+        // (g, kk = kp_rel - g) that share it; the q/dO chunks of the tile's queries stay in registers.
+        constexpr int kNgrp = kNF / kC8;  // 8 (D=128) or 16 (D=64)
+        const int c8 = ft % kC8, grp = ft / kC8;
+        uint4 xq[4], ud[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          xq[g] = ud[g] = make_uint4(0u, 0u, 0u, 0u);
+          if (g < a.G && q0 + g < qb) {
+            xq[g] = *reinterpret_cast<const uint4*>(&sm.sq[buf][g][8 * c8]);
+            ud[g] = *reinterpret_cast<const uint4*>(&sm.sdo[buf][g][8 * c8]);
+          }
+        }
+        const int nkr = a.R + a.G - 1;
+        for (int kr = grp; kr < nkr; kr += kNgrp) {
+          const int kpos = kbase + kr;
+          int slot = sbase + kr;
+          if (slot >= a.ring) slot -= a.ring;
+          uint4 yk = make_uint4(0u, 0u, 0u, 0u), wv = yk;
+          if (kpos >= 0) {
+            yk = *reinterpret_cast<const uint4*>(&sm.rk2[slot][8 * c8]);
+            wv = *reinterpret_cast<const uint4*>(&sm.rv2[slot][8 * c8]);
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int kk = kr - g;
+            if (g >= a.G || kk < 0 || kk >= a.R) continue;
+            const bool ok = q0 + g < qb && kpos >= 0;
+            uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
+            if (ok) {
+              oa = make_uint4(hmul2_u32(xq[g].x, yk.x), hmul2_u32(xq[g].y, yk.y), hmul2_u32(xq[g].z, yk.z),
+                              hmul2_u32(xq[g].w, yk.w));
+              od = make_uint4(hmul2_u32(ud[g].x, wv.x), hmul2_u32(ud[g].y, wv.y), hmul2_u32(ud[g].z, wv.z),
+                              hmul2_u32(ud[g].w, wv.w));
+            }
+            const uint32_t dst = sw128_off((g << a.lR) + kk, c8);
+            *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
+            *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
+          }
+        }
+        // rows r >= G*R (R not dividing 128) stay zero from the previous fill: clear them explicitly
+        for (int r = a.G * a.R + grp; r < 128; r += kNgrp) {
+          const uint32_t dst = sw128_off(r, c8);
+          *reinterpret_cast<uint4*>(sm.as[buf] + dst) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = make_uint4(0u, 0u, 0u, 0u);
+        }
+      } else if (!DET) {
         // trilinear: thread -> (16-byte column chunk c8, block of kRB consecutive rows), 4 rows in
         // flight at a time; the q/dO chunk is reloaded only when the row's query changes
         constexpr int kRB = 128 * kC8 / kNF;  // rows per thread: 16 (D=128) or 8 (D=64)
@@ -1162,6 +1214,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.aready[buf]);
+      SA_TRACE_AT(trf, 3, trn, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
   } else if (warp == 12) {
@@ -1172,10 +1225,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
       const uint32_t kaddr = smem_u32(sm.kb), vaddr = smem_u32(sm.vb);
       mbar_wait(&sm.kvload, 0);
+      int trn = 0;
       for (int t = 0; t < ntile; ++t) {
         const int buf = t & 1;
+        const bool trm = lane == 0 && t >= 50 && t < 53;
         mbar_wait(&sm.aready[buf], (t >> 1) & 1);
         tc_fence_after();
+        SA_TRACE_AT(trm, 4, trn, t << 16 | 40 << 8);
         const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -1202,6 +1258,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             mma_ts_w(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
           }
         }
+        SA_TRACE_AT(trm, 4, trn, t << 16 | 41 << 8);
         mma_commit_w(&sm.afree[buf]);
       }
       mma_commit_w(&sm.done);
@@ -1216,11 +1273,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     const int jw0 = j0 + qd * 32;          // warp's first key row
     const int cb = 64 * half;              // tile columns (rows (i,k)) handled by this half
     const float sl2 = p.scale * kLog2e;
+    int trn = 0;
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
       const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
+      const bool trs = (threadIdx.x & 127) == 0 && t >= 50 && t < 53;
       mbar_wait(&sm.sfull[half], t & 1);
       tc_fence_after();
+      SA_TRACE_AT(trs, 5 + half, trn, t << 16 | (50 + half) << 8);
       // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
       // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
       const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
@@ -1263,6 +1323,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.pready[half]);
+      SA_TRACE_AT(trs, 5 + half, trn, t << 16 | (54 + half) << 8);
     }
     // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns; dK carries the scale s
     if (ntile > 0) {
