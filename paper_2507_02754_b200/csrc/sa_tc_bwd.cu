@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         named_bar_sync(1, 256);
       }
+      SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 8 << 8);
       const bool first_in_sub = item == it_begin || it.grp == 0;
       const bool last_in_sub = item == it_end - 1 || it.grp == a.ngroups - 1;
       const int P0 = p.np + it.i0;
@@ -676,6 +677,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
             }
           }
         }
+        SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 9 << 8);
         tmem_store_row<D>(half == 0 ? tAS : tAdP, pk);
         tmem_st_wait();
         tc_fence_before();
@@ -860,7 +862,9 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
 // exponent and the dK epilogue) are formed by 3 former warps from an fp16 staging ring filled
 // with cp.async one tile ahead.
 // ==========================================================================================
-constexpr int kKVThreads = 416;  // warps 0-7 softmax-gradient, 8-11 A-tile formers (8 also TMA), 12 MMA
+constexpr int kKVFW = 8;                      // A-tile former warps (the first one also issues the TMA)
+constexpr int kKVWarpMMA = 8 + kKVFW;
+constexpr int kKVThreads = 32 * (kKVWarpMMA + 1);  // warps 0-7 softmax-gradient, 8.. formers, last MMA
 constexpr uint32_t kKST = 0, kKdPT = 128, kKdV = 256, kKdK = 384;
 constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
 constexpr int kKVGmax = 8;    // staged queries per tile
@@ -921,7 +925,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     tma_prefetch(&tmV);
     mbar_init(&sm.kvload, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&sm.aready[s], 4);
+      mbar_init(&sm.aready[s], kKVFW);
       mbar_init(&sm.afree[s], 1);
       mbar_init(&sm.sfull[s], 1);
       mbar_init(&sm.pready[s], 4);
@@ -929,13 +933,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     mbar_init(&sm.done, 1);
     fence_mbar_init();
   }
-  if (warp == 12) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == kKVWarpMMA) tmem_alloc<512>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
-  if (warp >= 8 && warp <= 11) {
+  if (warp >= 8 && warp < kKVWarpMMA) {
     // ------------------------------ TMA (once) + A-tile formers ------------------------------
     if (warp == 8 && lane == 0 && ntile > 0) {
       mbar_expect_tx(&sm.kvload, 2 * KVSmem<D>::kTileBytes);
@@ -944,8 +948,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         tma_load_4d(sm.vb + pn * kPanelBytes, &tmV, &sm.kvload, pn * 64, h, j0, b);
       }
     }
-    const int ft = (warp - 8) * 32 + lane;  // 0..127
-    constexpr int kNF = 128;
+    const int ft = (warp - 8) * 32 + lane;
+    constexpr int kNF = 32 * kKVFW;
     // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
     auto ring_mod = [&](int kp) {  // kp mod ring for kp >= -ring (one division per call site)
       return (kp + a.ring) % a.ring;
@@ -1217,7 +1221,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       SA_TRACE_AT(trf, 3, trn, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
-  } else if (warp == 12) {
+  } else if (warp == kKVWarpMMA) {
     // ------------------------------ MMA issuer ------------------------------
     if (ntile > 0) {  // whole warp; elected lane issues
       const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
@@ -1379,7 +1383,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 
   __syncthreads();
   tc_fence_after();
-  if (warp == 12) tmem_free<512>(tbase);
+  if (warp == kKVWarpMMA) tmem_free<512>(tbase);
 }
 
 }  // namespace

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_sync(3, 256);
       }
+      SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 28 << 8);
       const int i0 = (2 * it.pair + x) * a.G;
       const int nq = max(0, min(a.G, p.N - i0));
       const bool row_in = r < a.G * a.R && g < nq;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
         if (valid) row_operand_f16<D>(qrow, k2row, a.a_scale, p.det, pk);
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 29 << 8);
         tmem_store_row<D>(tA, pk);
         tmem_st_wait();
         tc_fence_before();
