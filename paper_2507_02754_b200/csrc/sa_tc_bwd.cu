@@ -713,12 +713,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
           const bool need_mask = lo_c > 0 || hi_c < 31;
           uint32_t pp[16], pd[16];
           if (!__any_sync(0xffffffffu, need_mask)) {
+            const float2 vs = make_float2(sl2, sl2), vl = make_float2(-lse_l2, -lse_l2), vd = make_float2(-dl, -dl);
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-              const float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), sl2, -lse_l2));
-              const float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), sl2, -lse_l2));
-              pp[t] = pack_f16x2(p0, p1);
-              pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
+              const float2 x = ffma2(make_float2(__uint_as_float(su[2 * t]), __uint_as_float(su[2 * t + 1])), vs, vl);
+              const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+              pp[t] = pack_f16x2(pv);
+              pd[t] = pack_f16x2(
+                  fmul2(pv, fadd2(make_float2(__uint_as_float(du[2 * t]), __uint_as_float(du[2 * t + 1])), vd)));
             }
           } else {
 #pragma unroll
@@ -1300,6 +1302,9 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       // two 32-column steps (register pressure); P^T / dS^T of this half go to the first 32
       // columns of the half's own S^T / dP^T region (columns already consumed)
+      // fast path: every column of a 32-column step belongs to one query (R >= 32), no column is
+      // masked and no row precedes the sequence start -> one (lse, delta) pair per step, packed math
+      const bool fast = all_in && a.R >= 32 && P0 - a.R + 1 >= 0;
 #pragma unroll
       for (int sub = 0; sub < 2; ++sub) {
         uint32_t su[32], du[32];
@@ -1307,6 +1312,21 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         tmem_ld32(tdPT + cb + 32 * sub, du);
         tmem_ld_wait();
         uint32_t pp[16], pd[16];
+        if (fast) {
+          const float2 ri = sm.rinfo[buf][cb + 32 * sub];
+          const float2 vs = make_float2(sl2, sl2), vl = make_float2(-ri.x, -ri.x), vd = make_float2(-ri.y, -ri.y);
+#pragma unroll
+          for (int t2 = 0; t2 < 16; ++t2) {
+            const float2 x = ffma2(make_float2(__uint_as_float(su[2 * t2]), __uint_as_float(su[2 * t2 + 1])), vs, vl);
+            const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+            pp[t2] = pack_f16x2(pv);
+            pd[t2] = pack_f16x2(
+                fmul2(pv, fadd2(make_float2(__uint_as_float(du[2 * t2]), __uint_as_float(du[2 * t2 + 1])), vd)));
+          }
+          tmem_st16(tST + cb + 16 * sub, pp);
+          tmem_st16(tdPT + cb + 16 * sub, pd);
+          continue;
+        }
 #pragma unroll
         for (int t2 = 0; t2 < 16; ++t2) {
           const int c = 32 * sub + 2 * t2;
