@@ -857,23 +857,30 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
 
 // ==========================================================================================
 // bwd_kv: dK, dV (K/V-stationary).  TMEM lanes = key rows j of the CTA's 128-row block.
-// The row tile's columns are processed in two halves (tile rows 0-63 / 64-127) so that the
-// softmax-gradient of one half overlaps the MMAs of the other:
-//   S^T_a, dP^T_a | S^T_b, dP^T_b | (P_a ready) dV,dK += half a | (P_b ready) dV,dK += half b
+// The CTA's K and V rows sit in TMEM as fp16 A operands for the whole launch, so every MMA is a
+// TS-MMA (SMEM reads <= 64 B/clk, leaving SMEM bandwidth for the A-tile formers; an SS-MMA at
+// N=64 saturates SMEM at 128 B/clk, tools/micro/mma_rate.cu).  The row tile's 128 columns are
+// processed in quarters of 32 (double-buffered S^T/dP^T in TMEM), issued as
+//   S^T,dP^T(Q) | S^T,dP^T(Q+1) | [P(Q) ready] dV,dK += quarter Q ; S^T,dP^T(Q+2) | ...
+// so the softmax-gradient of quarter Q (warpgroup Q%2) overlaps the MMAs of quarter Q+1.
 // A tiles (A_S = q o k2 [det k2 x q], A_dP = dO o v2, fp16, unscaled: s is folded into the
-// exponent and the dK epilogue) are formed by 3 former warps from an fp16 staging ring filled
-// with cp.async one tile ahead.
+// exponent and the dK epilogue) are formed into SMEM by the former warps from an fp16 staging
+// ring filled with cp.async one tile ahead.
 // ==========================================================================================
-constexpr int kKVFW = 8;                      // A-tile former warps (the first one also issues the TMA)
+constexpr int kKVFW = 8;                      // A-tile former warps
+constexpr int kKVF0 = 0;                      // first former warp (low ids: issue priority)
+constexpr int kKVS0 = kKVFW;                  // first softmax-gradient warp (8 warps)
 constexpr int kKVWarpMMA = 8 + kKVFW;
 constexpr int kKVThreads = 32 * (kKVWarpMMA + 1);  // warps 0-7 softmax-gradient, 8.. formers, last MMA
-constexpr uint32_t kKST = 0, kKdPT = 128, kKdV = 256, kKdK = 384;
+// TMEM columns: K, V operands (D/2 packed cols each), dV, dK accumulators, 2 x (S^T, dP^T) quarters
+constexpr uint32_t kKK = 0, kKV = 64, kKdV = 128, kKdK = 256, kKSD = 384;
 constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
 constexpr int kKVGmax = 8;    // staged queries per tile
 
 struct BwdKVArgs {
   Problem p;  // after the swap: w1 = long window (this kernel's keys), w2 = R
   const __half *q, *k2, *v2, *dO;  // fp16 copies
+  const __half *k, *v;             // fp16 copies of this kernel's stationary keys
   const float *lse, *delta;
   void *dk, *dv;
   int out_f32, R, lR, G, ring;
@@ -883,8 +890,6 @@ template <int D>
 struct KVSmem {
   static constexpr int kPanelBytes = 128 * 128;  // 128 rows x 64 fp16
   static constexpr int kTileBytes = 128 * D * 2;
-  alignas(1024) uint8_t kb[kTileBytes];
-  alignas(1024) uint8_t vb[kTileBytes];
   alignas(1024) uint8_t as[2][kTileBytes];
   alignas(1024) uint8_t adp[2][kTileBytes];
   alignas(16) __half rk2[kKVRing][D];
@@ -893,7 +898,7 @@ struct KVSmem {
   alignas(16) __half sdo[2][kKVGmax][D];
   float slse[2][kKVGmax], sdl[2][kKVGmax];
   float2 rinfo[2][128];  // (lse * log2e or +inf for invalid rows, delta)
-  uint64_t kvload, aready[2], afree[2], sfull[2], pready[2], done;
+  uint64_t kvtm, aready[2], afree[2], sfull[2], pready[2], done;
   uint32_t tmem_base;
 };
 
@@ -906,7 +911,7 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int c8) {
 
 template <int D, bool DET, bool STAGED>
 __global__ void __launch_bounds__(kKVThreads, 1)
-    tc_bwd_kv_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdKVArgs a) {
+    tc_bwd_kv_kernel(BwdKVArgs a) {
   extern __shared__ uint8_t smem_raw[];
   static_assert(sizeof(KVSmem<D>) + 1024 <= 232448, "shared memory budget");
   KVSmem<D>& sm = *reinterpret_cast<KVSmem<D>*>(smem_raw + align1024_pad(smem_raw));
@@ -923,9 +928,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   const int ntile = qb > qa ? (qb - qa + a.G - 1) / a.G : 0;
 
   if (warp == 8 && lane == 0) {
-    tma_prefetch(&tmK);
-    tma_prefetch(&tmV);
-    mbar_init(&sm.kvload, 1);
+    mbar_init(&sm.kvtm, 8);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.aready[s], kKVFW);
       mbar_init(&sm.afree[s], 1);
@@ -941,16 +944,9 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, sm.tmem_base, 0);  // provably warp-uniform
 
-  if (warp >= 8 && warp < kKVWarpMMA) {
-    // ------------------------------ TMA (once) + A-tile formers ------------------------------
-    if (warp == 8 && lane == 0 && ntile > 0) {
-      mbar_expect_tx(&sm.kvload, 2 * KVSmem<D>::kTileBytes);
-      for (int pn = 0; pn < kPanels; ++pn) {
-        tma_load_4d(sm.kb + pn * kPanelBytes, &tmK, &sm.kvload, pn * 64, h, j0, b);
-        tma_load_4d(sm.vb + pn * kPanelBytes, &tmV, &sm.kvload, pn * 64, h, j0, b);
-      }
-    }
-    const int ft = (warp - 8) * 32 + lane;
+  if (warp >= kKVF0 && warp < kKVF0 + kKVFW) {
+    // ------------------------------ A-tile formers ------------------------------
+    const int ft = (warp - kKVF0) * 32 + lane;
     constexpr int kNF = 32 * kKVFW;
     // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
     auto ring_mod = [&](int kp) {  // kp mod ring for kp >= -ring (one division per call site)
@@ -1031,11 +1027,50 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         sm.rinfo[buf][r] = ri;
       }
+      SA_TRACE_AT(trf, 3, trn, t << 16 | 33 << 8);
       // A_S = q o k2 [det: k2 x q], A_dP = dO o v2 -> swizzled fp16 tiles
       constexpr int kWS = DET ? 24 : 8;       // A_S task width (elements)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
-      if (!DET && STAGED && a.G <= 4) {
+      constexpr int kRB8 = 128 * kC8 / kNF;  // rows per thread in the row-block mapping (8 at D=128)
+      if (!DET && STAGED && a.R >= kRB8) {
+        // trilinear, row blocks: thread -> (column chunk c8, kRB8 consecutive tile rows of ONE query).
+        // All loads first, then the products and the stores: no branches, kRB8-way ILP.
+        const int c8 = ft % kC8, r0 = (ft / kC8) * kRB8;
+        const int g = r0 >> a.lR, kk0 = r0 & (a.R - 1);
+        const bool qok = r0 < a.G * a.R && q0 + g < qb;
+        uint4 xq = make_uint4(0u, 0u, 0u, 0u), ud = xq;
+        if (qok) {
+          xq = *reinterpret_cast<const uint4*>(&sm.sq[buf][g][8 * c8]);
+          ud = *reinterpret_cast<const uint4*>(&sm.sdo[buf][g][8 * c8]);
+        }
+        uint4 yk[kRB8], wv[kRB8];
+        int slot = sbase + g + kk0;
+        if (slot >= a.ring) slot -= a.ring;
+#pragma unroll
+        for (int u = 0; u < kRB8; ++u) {
+          const bool ok = qok && kbase + g + kk0 + u >= 0;
+          int su = slot + u;
+          if (su >= a.ring) su -= a.ring;
+          yk[u] = wv[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (ok) {
+            yk[u] = *reinterpret_cast<const uint4*>(&sm.rk2[su][8 * c8]);
+            wv[u] = *reinterpret_cast<const uint4*>(&sm.rv2[su][8 * c8]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kRB8; ++u) {
+          const uint4 oa = make_uint4(hmul2_u32(xq.x, yk[u].x), hmul2_u32(xq.y, yk[u].y), hmul2_u32(xq.z, yk[u].z),
+                                      hmul2_u32(xq.w, yk[u].w));
+          const uint4 od = make_uint4(hmul2_u32(ud.x, wv[u].x), hmul2_u32(ud.y, wv[u].y), hmul2_u32(ud.z, wv[u].z),
+                                      hmul2_u32(ud.w, wv[u].w));
+          const uint32_t dst = sw128_off(r0 + u, c8);
+          *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
+          *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
+        }
+        SA_TRACE_AT(trf, 3, trn, t << 16 | 34 << 8);
+        SA_TRACE_AT(trf, 3, trn, t << 16 | 35 << 8);
+      } else if (!DET && STAGED && a.G <= 4) {
         // trilinear, key-row major: thread -> (column chunk c8, key rows kp_rel = grp, grp+ngrp, ...).
         // Each staged k2/v2 chunk is read once and multiplied into the (up to G) tile rows
         // (g, kk = kp_rel - g) that share it; the q/dO chunks of the tile's queries stay in registers.
@@ -1051,6 +1086,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           }
         }
         const int nkr = a.R + a.G - 1;
+        SA_TRACE_AT(trf, 3, trn, t << 16 | 34 << 8);
         for (int kr = grp; kr < nkr; kr += kNgrp) {
           const int kpos = kbase + kr;
           int slot = sbase + kr;
@@ -1077,6 +1113,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
           }
         }
+        SA_TRACE_AT(trf, 3, trn, t << 16 | 35 << 8);
         // rows r >= G*R (R not dividing 128) stay zero from the previous fill: clear them explicitly
         for (int r = a.G * a.R + grp; r < 128; r += kNgrp) {
           const uint32_t dst = sw128_off(r, c8);
@@ -1226,129 +1263,155 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   } else if (warp == kKVWarpMMA) {
     // ------------------------------ MMA issuer ------------------------------
     if (ntile > 0) {  // whole warp; elected lane issues
-      const uint32_t tST = tbase + kKST, tdPT = tbase + kKdPT, tdV = tbase + kKdV, tdK = tbase + kKdK;
-      const uint32_t idesc_s = idesc_f16(128, 64, 0, 0);
+      const uint32_t tK = tbase + kKK, tV = tbase + kKV, tdV = tbase + kKdV, tdK = tbase + kKdK;
+      const uint32_t tSD = tbase + kKSD;
+      const uint32_t idesc_s = idesc_f16(128, 32, 0, 0);
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
-      const uint32_t kaddr = smem_u32(sm.kb), vaddr = smem_u32(sm.vb);
-      mbar_wait(&sm.kvload, 0);
+      const int nquart = 4 * ntile;
+      mbar_wait(&sm.kvtm, 0);
+      tc_fence_after();
       int trn = 0;
-      for (int t = 0; t < ntile; ++t) {
-        const int buf = t & 1;
-        const bool trm = lane == 0 && t >= 50 && t < 53;
-        mbar_wait(&sm.aready[buf], (t >> 1) & 1);
-        tc_fence_after();
-        SA_TRACE_AT(trm, 4, trn, t << 16 | 40 << 8);
+      // S^T = K A_S^T and dP^T = V A_dP^T for tile rows [32q, 32q+32) into buffer Q&1
+      auto issue_s = [&](int Q) {
+        const int t = Q >> 2, q = Q & 3, buf = t & 1, sb = Q & 1;
+        if (q == 0) {
+          mbar_wait(&sm.aready[buf], (t >> 1) & 1);
+          tc_fence_after();
+          SA_TRACE_AT(lane == 0 && t >= 50 && t < 53, 4, trn, t << 16 | 40 << 8);
+        }
         const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
-            const uint32_t boff = off + hh * 64 * 128;
-            mma_ss_w(tST + 64 * hh, smem_desc_sw128(kaddr + off, 16, 1024), smem_desc_sw128(asa + boff, 16, 1024),
-                   idesc_s, kk > 0 ? 1u : 0u);
-            mma_ss_w(tdPT + 64 * hh, smem_desc_sw128(vaddr + off, 16, 1024), smem_desc_sw128(ada + boff, 16, 1024),
-                   idesc_s, kk > 0 ? 1u : 0u);
-          }
-          mma_commit_w(&sm.sfull[hh]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + q * 32 * 128;
+          mma_ts_w(tSD + 64 * sb, tK + kk * 8, smem_desc_sw128(asa + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          mma_ts_w(tSD + 64 * sb + 32, tV + kk * 8, smem_desc_sw128(ada + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
+        mma_commit_w(&sm.sfull[sb]);
+      };
+      issue_s(0);
+      if (nquart > 1) issue_s(1);
+      for (int Q = 0; Q < nquart; ++Q) {
+        const int t = Q >> 2, q = Q & 3, buf = t & 1, sb = Q & 1;
+        mbar_wait(&sm.pready[sb], (Q >> 1) & 1);
+        tc_fence_after();
+        const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          mbar_wait(&sm.pready[hh], t & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t acc = (t > 0 || hh > 0 || kk > 0) ? 1u : 0u;
-            const uint32_t roff = (64 * hh + 16 * kk) * 128;
-            mma_ts_w(tdV, tST + 64 * hh + 8 * kk, smem_desc_sw128(ada + roff, kPanelBytes, 1024), idesc_acc, acc);
-            mma_ts_w(tdK, tdPT + 64 * hh + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
-          }
+        for (int kk = 0; kk < 2; ++kk) {  // dV += P^T A_dP, dK += dS^T A_S over the quarter's 32 rows
+          const uint32_t acc = (Q > 0 || kk > 0) ? 1u : 0u;
+          const uint32_t roff = (32 * q + 16 * kk) * 128;
+          mma_ts_w(tdV, tSD + 64 * sb + 8 * kk, smem_desc_sw128(ada + roff, kPanelBytes, 1024), idesc_acc, acc);
+          mma_ts_w(tdK, tSD + 64 * sb + 32 + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
         }
-        SA_TRACE_AT(trm, 4, trn, t << 16 | 41 << 8);
-        mma_commit_w(&sm.afree[buf]);
+        if (q == 3) {
+          mma_commit_w(&sm.afree[buf]);
+          SA_TRACE_AT(lane == 0 && t >= 50 && t < 53, 4, trn, t << 16 | 41 << 8);
+        }
+        // quarters of the next tile wait for its A tiles; issue them only after this tile's last
+        // dV/dK MMAs so that afree(t) never waits on the formation of tile t+1
+        if (q < 2) {
+          if (Q + 2 < nquart) issue_s(Q + 2);
+        } else if (q == 3) {
+          if (Q + 1 < nquart) issue_s(Q + 1);
+          if (Q + 2 < nquart) issue_s(Q + 2);
+        }
       }
       mma_commit_w(&sm.done);
     }
-  } else if (warp < 8) {
+  } else if (warp != kKVWarpMMA) {
     // ------------------------------ P^T, dS^T and the dK/dV epilogue ------------------------------
-    const int qd = warp & 3, half = warp >> 2;
+    const int qd = warp & 3, wg = (warp - kKVS0) >> 2;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
-    const uint32_t tST = tbase + kKST + lane_off, tdPT = tbase + kKdPT + lane_off;
+    const uint32_t tS = tbase + kKSD + 64 * wg + lane_off, tdP = tS + 32;
     const uint32_t tdV = tbase + kKdV + lane_off, tdK = tbase + kKdK + lane_off;
     const int j = j0 + qd * 32 + lane;     // this thread's key row
     const int jw0 = j0 + qd * 32;          // warp's first key row
-    const int cb = 64 * half;              // tile columns (rows (i,k)) handled by this half
     const float sl2 = p.scale * kLog2e;
-    int trn = 0;
-    for (int t = 0; t < ntile; ++t) {
-      const int buf = t & 1;
-      const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
-      const bool trs = (threadIdx.x & 127) == 0 && t >= 50 && t < 53;
-      mbar_wait(&sm.sfull[half], t & 1);
-      tc_fence_after();
-      SA_TRACE_AT(trs, 5 + half, trn, t << 16 | (50 + half) << 8);
-      // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
-      // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
-      const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
-      int clo = 0, chi = 127;
-      if (!all_in) {
-        const int glo = max(0, j - P0), ghi = min(a.G - 1, j - P0 + p.w1 - 1);
-        clo = glo * a.R - cb;
-        chi = (ghi + 1) * a.R - 1 - cb;
-        if (ghi < glo) {
-          clo = 1;
-          chi = 0;
+    // K (warpgroup 0) / V (warpgroup 1) rows of this CTA -> TMEM fp16 A operands (zero past NK)
+    {
+      uint32_t pk[D / 2];
+#pragma unroll
+      for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
+      if (j < p.NK()) {
+        const uint4* src = reinterpret_cast<const uint4*>((wg == 0 ? a.k : a.v) + p.koff(b, j, h));
+#pragma unroll
+        for (int t = 0; t < D / 8; ++t) {
+          const uint4 x = src[t];
+          pk[4 * t] = x.x;
+          pk[4 * t + 1] = x.y;
+          pk[4 * t + 2] = x.z;
+          pk[4 * t + 3] = x.w;
         }
       }
-      // two 32-column steps (register pressure); P^T / dS^T of this half go to the first 32
-      // columns of the half's own S^T / dP^T region (columns already consumed)
-      // fast path: every column of a 32-column step belongs to one query (R >= 32), no column is
-      // masked and no row precedes the sequence start -> one (lse, delta) pair per step, packed math
-      const bool fast = all_in && a.R >= 32 && P0 - a.R + 1 >= 0;
-#pragma unroll
-      for (int sub = 0; sub < 2; ++sub) {
-        uint32_t su[32], du[32];
-        tmem_ld32(tST + cb + 32 * sub, su);
-        tmem_ld32(tdPT + cb + 32 * sub, du);
-        tmem_ld_wait();
-        uint32_t pp[16], pd[16];
-        if (fast) {
-          const float2 ri = sm.rinfo[buf][cb + 32 * sub];
-          const float2 vs = make_float2(sl2, sl2), vl = make_float2(-ri.x, -ri.x), vd = make_float2(-ri.y, -ri.y);
-#pragma unroll
-          for (int t2 = 0; t2 < 16; ++t2) {
-            const float2 x = ffma2(make_float2(__uint_as_float(su[2 * t2]), __uint_as_float(su[2 * t2 + 1])), vs, vl);
-            const float2 pv = make_float2(ex2(x.x), ex2(x.y));
-            pp[t2] = pack_f16x2(pv);
-            pd[t2] = pack_f16x2(
-                fmul2(pv, fadd2(make_float2(__uint_as_float(du[2 * t2]), __uint_as_float(du[2 * t2 + 1])), vd)));
-          }
-          tmem_st16(tST + cb + 16 * sub, pp);
-          tmem_st16(tdPT + cb + 16 * sub, pd);
-          continue;
-        }
-#pragma unroll
-        for (int t2 = 0; t2 < 16; ++t2) {
-          const int c = 32 * sub + 2 * t2;
-          const float2 r0 = sm.rinfo[buf][cb + c], r1 = sm.rinfo[buf][cb + c + 1];
-          float p0 = ex2(fmaf(__uint_as_float(su[2 * t2]), sl2, -r0.x));
-          float p1 = ex2(fmaf(__uint_as_float(su[2 * t2 + 1]), sl2, -r1.x));
-          if (!all_in) {
-            p0 = (c >= clo && c <= chi) ? p0 : 0.f;
-            p1 = (c + 1 >= clo && c + 1 <= chi) ? p1 : 0.f;
-          }
-          pp[t2] = pack_f16x2(p0, p1);
-          pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[2 * t2]) - r0.y), p1 * (__uint_as_float(du[2 * t2 + 1]) - r1.y));
-        }
-        tmem_st16(tST + cb + 16 * sub, pp);
-        tmem_st16(tdPT + cb + 16 * sub, pd);
-      }
+      tmem_store_row<D>(tbase + (wg == 0 ? kKK : kKV) + lane_off, pk);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.pready[half]);
-      SA_TRACE_AT(trs, 5 + half, trn, t << 16 | (54 + half) << 8);
+      if (lane == 0) mbar_arrive(&sm.kvtm);
     }
+    int trn = 0;
+    const int nquart = 4 * ntile;
+    for (int Q = wg; Q < nquart; Q += 2) {
+      const int t = Q >> 2, q = Q & 3, buf = t & 1;
+      const int cb = 32 * q;               // tile columns (rows (i,k)) of this quarter
+      const int P0 = p.np + qa + t * a.G;  // key position of the tile's first query
+      const bool trs = (threadIdx.x & 127) == 0 && t >= 50 && t < 53;
+      mbar_wait(&sm.sfull[wg], (Q >> 1) & 1);
+      tc_fence_after();
+      SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (50 + q) << 8);
+      // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
+      // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
+      const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
+      // fast path: the quarter's 32 columns belong to one query (R >= 32), no column is masked and no
+      // row precedes the sequence start -> one (lse, delta) pair, packed math
+      const bool fast = all_in && a.R >= 32 && P0 - a.R + 1 >= 0;
+      uint32_t su[32], du[32];
+      tmem_ld32(tS, su);
+      tmem_ld32(tdP, du);
+      tmem_ld_wait();
+      uint32_t pp[16], pd[16];
+      if (fast) {
+        const float2 ri = sm.rinfo[buf][cb];
+        const float2 vs = make_float2(sl2, sl2), vl = make_float2(-ri.x, -ri.x), vd = make_float2(-ri.y, -ri.y);
+#pragma unroll
+        for (int t2 = 0; t2 < 16; ++t2) {
+          const float2 x = ffma2(make_float2(__uint_as_float(su[2 * t2]), __uint_as_float(su[2 * t2 + 1])), vs, vl);
+          const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+          pp[t2] = pack_f16x2(pv);
+          pd[t2] = pack_f16x2(
+              fmul2(pv, fadd2(make_float2(__uint_as_float(du[2 * t2]), __uint_as_float(du[2 * t2 + 1])), vd)));
+        }
+      } else {
+        int clo = 0, chi = 31;
+        if (!all_in) {
+          const int glo = max(0, j - P0), ghi = min(a.G - 1, j - P0 + p.w1 - 1);
+          clo = glo * a.R - cb;
+          chi = (ghi + 1) * a.R - 1 - cb;
+          if (ghi < glo) {
+            clo = 1;
+            chi = 0;
+          }
+        }
+#pragma unroll
+        for (int t2 = 0; t2 < 16; ++t2) {
+          const int c = 2 * t2;
+          const float2 r0 = sm.rinfo[buf][cb + c], r1 = sm.rinfo[buf][cb + c + 1];
+          float p0 = ex2(fmaf(__uint_as_float(su[c]), sl2, -r0.x));
+          float p1 = ex2(fmaf(__uint_as_float(su[c + 1]), sl2, -r1.x));
+          p0 = (c >= clo && c <= chi) ? p0 : 0.f;
+          p1 = (c + 1 >= clo && c + 1 <= chi) ? p1 : 0.f;
+          pp[t2] = pack_f16x2(p0, p1);
+          pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[c]) - r0.y), p1 * (__uint_as_float(du[c + 1]) - r1.y));
+        }
+      }
+      tmem_st16(tS, pp);
+      tmem_st16(tdP, pd);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.pready[wg]);
+      SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (54 + q) << 8);
+    }
+    const int half = wg;
     // epilogue: dV, dK rows (lane = key row j), this half's D/2 columns; dK carries the scale s
     if (ntile > 0) {
       mbar_wait(&sm.done, 0);
@@ -1555,16 +1618,14 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
 
   // bwd_kv: dk, dv
   {
-    CUtensorMap tmK, tmV;
-    if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.H, p.D, 128) ||
-        !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.H, p.D, 128))
-      return cudaErrorInvalidValue;
     BwdKVArgs a;
     a.p = p;
     a.q = (const __half*)qf;
     a.k2 = (const __half*)k2f;
     a.v2 = (const __half*)v2f;
     a.dO = (const __half*)dof;
+    a.k = (const __half*)kf;
+    a.v = (const __half*)vf;
     a.lse = lse;
     a.delta = delta;
     a.dk = dk;
@@ -1579,7 +1640,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     auto launch = [&](auto kern, size_t smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       KernelScope ks("tc_bwd_kv", st);
-      kern<<<grid, kKVThreads, smem, st>>>(tmK, tmV, a);
+      kern<<<grid, kKVThreads, smem, st>>>(a);
     };
     const size_t s128 = sizeof(KVSmem<128>) + 1024, s64 = sizeof(KVSmem<64>) + 1024;
     if (p.D == 128) {
