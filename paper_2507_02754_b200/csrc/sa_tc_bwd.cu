@@ -1290,6 +1290,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       };
       issue_s(0);
       if (nquart > 1) issue_s(1);
+      bool early = false;
       for (int Q = 0; Q < nquart; ++Q) {
         const int t = Q >> 2, q = Q & 3, buf = t & 1, sb = Q & 1;
         mbar_wait(&sm.pready[sb], (Q >> 1) & 1);
@@ -1308,10 +1309,14 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         // quarters of the next tile wait for its A tiles; issue them only after this tile's last
         // dV/dK MMAs so that afree(t) never waits on the formation of tile t+1
+        // (issued early, after quarter 2, when the next tile's A tiles are already formed)
         if (q < 2) {
           if (Q + 2 < nquart) issue_s(Q + 2);
-        } else if (q == 3) {
-          if (Q + 1 < nquart) issue_s(Q + 1);
+        } else if (q == 2) {
+          early = Q + 2 < nquart && mbar_test(&sm.aready[buf ^ 1], ((t + 1) >> 1) & 1);
+          if (early) issue_s(Q + 2);
+        } else {
+          if (!early && Q + 1 < nquart) issue_s(Q + 1);
           if (Q + 2 < nquart) issue_s(Q + 2);
         }
       }
@@ -1368,6 +1373,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tmem_ld32(tS, su);
       tmem_ld32(tdP, du);
       tmem_ld_wait();
+      SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (60 + q) << 8);
       uint32_t pp[16], pd[16];
       if (fast) {
         const float2 ri = sm.rinfo[buf][cb];
@@ -1403,6 +1409,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           pd[t2] = pack_f16x2(p0 * (__uint_as_float(du[c]) - r0.y), p1 * (__uint_as_float(du[c + 1]) - r1.y));
         }
       }
+      SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (64 + q) << 8);
       tmem_st16(tS, pp);
       tmem_st16(tdP, pd);
       tmem_st_wait();
