@@ -38,10 +38,6 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMaxR = 64;  // bwd_q: rows per query (folded window w2) supported by the ring
 constexpr int kRingMax = 66;
 
-__device__ __forceinline__ uint32_t hmul2_u32(uint32_t x, uint32_t y) {
-  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&x), *reinterpret_cast<__half2*>(&y));
-  return *reinterpret_cast<uint32_t*>(&r);
-}
 
 // ------------------------------------------------------------------------------------------
 // delta_i = <dO_i, o_i>, one warp per query row
@@ -759,8 +755,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
           q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256);
       } else if (a.R == 32) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < D; c0 += 32)
+        for (int c0 = 0; c0 < D; c0 += 32) {
           q_epilogue_pass32<D, RING, STAGED>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
+          SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | (c0 / 32));
+        }
       } else {
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 16)

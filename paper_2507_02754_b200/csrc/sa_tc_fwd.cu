@@ -22,6 +22,8 @@ namespace sa {
 
 cudaError_t convert_pair_f16(const void* a, void* ao, const void* b, void* bo, int64_t n, int num_sms,
                              cudaStream_t st);
+cudaError_t convert_two_f16(const void* a, void* ao, int64_t na, const void* b, void* bo, int64_t nb, int num_sms,
+                            cudaStream_t st);
 int num_sms();
 
 namespace {
@@ -49,15 +51,33 @@ constexpr int kStgRows = 96;  // staged rows per pair (2G + 2(R+2G-1) <= 96: R i
 
 struct FwdArgs {
   Problem p;                // after the (K,V,w1) <-> (K',V',w2) swap: w2 = rows per query
-  const __nv_bfloat16* q;   // [B,N,H,D]
-  const __nv_bfloat16* k2;  // folded key (window w2), [B,NK,H,D]
+  const __half* q;          // fp16 copy, [B,N,H,D]
+  const __half* k2;         // fp16 copy of the folded key (window w2), [B,NK,H,D]
   const __nv_bfloat16* v2;
   void* o;
   float* lse;
   int out_f32;
   int R, G, ngroups, npairs, items;
-  float a_scale;  // s * log2(e), signed
+  float a_scale;  // s * log2(e), signed: applied to the det row operand
+  float sm_mult;  // softmax multiplier of the raw logits: s * log2(e) (trilinear, unscaled HMUL2 operand) or 1 (det)
 };
+
+// exp2 on the FMA pipe for a pair (FA4-style offload of part of the MUFU work): 2^x = 2^round(x) *
+// p(f), f = x - round(x) in [-1/2, 1/2], p the degree-3 relative-minimax fit (max rel err 1.0e-4,
+// below the fp16 rounding of P).  Arguments below -126 are clamped (result ~1e-38, not 0).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic rounds x into the low mantissa bits
+  x = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 j = fadd2(t, make_float2(-kMagic, -kMagic));
+  const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.055008301765721454f, 0.055008301765721454f), f,
+                   make_float2(0.2422094027065684f, 0.2422094027065684f));
+  p = ffma2(p, f, make_float2(0.6932828234305377f, 0.6932828234305377f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 
 template <int D>
 struct Smem {
@@ -225,15 +245,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nrows = 2 * a.G + 2 * nk2;
       for (int task = tid; task < nrows * kC8; task += 256) {
         const int row = task / kC8, c8 = task % kC8;
-        const __nv_bfloat16* src = nullptr;
+        const void* src = nullptr;
         if (row < 2 * a.G) {
-          if (i0 + row < p.N) src = a.q + p.qoff(it.b, i0 + row, it.h);
+          if (i0 + row < p.N) src = a.q + p.qoff(it.b, i0 + row, it.h) + 8 * c8;
         } else {
           const int rr = row - 2 * a.G;
           const int kp = kb + (rr < nk2 ? rr : rr - nk2);
-          if (kp >= 0 && kp < p.NK()) src = (rr < nk2 ? a.k2 : a.v2) + p.koff(it.b, kp, it.h);
+          if (kp >= 0 && kp < p.NK())
+            src = rr < nk2 ? (const void*)(a.k2 + p.koff(it.b, kp, it.h) + 8 * c8)
+                           : (const void*)(a.v2 + p.koff(it.b, kp, it.h) + 8 * c8);
         }
-        if (src) cp_async16(&sm.stg[buf][row][8 * c8], src + 8 * c8);
+        if (src) cp_async16(&sm.stg[buf][row][8 * c8], src);
       }
       cp_async_commit();
     };
@@ -263,8 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kpos = pos - a.R + 1 + kk;
       const bool valid = row_in && kpos >= 0;
       const int srow = x * a.G + g + kk;  // this row's k2/v2 staging offset
-      const __nv_bfloat16* qrow = STAGED ? &sm.stg[buf][x * a.G + g][0] : a.q + p.qoff(it.b, i0 + g, it.h);
-      const __nv_bfloat16* k2row = STAGED ? &sm.stg[buf][2 * a.G + srow][0] : a.k2 + p.koff(it.b, kpos, it.h);
+      const __half* qrow = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][x * a.G + g][0])
+                                  : a.q + p.qoff(it.b, i0 + g, it.h);
+      const __half* k2row = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][2 * a.G + srow][0])
+                                   : a.k2 + p.koff(it.b, kpos, it.h);
       const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2 + srow][0] : a.v2 + p.koff(it.b, kpos, it.h);
 
       // ---- A operand a_(i,k) = s log2e (q_i o k2_k)  [det: s log2e (k2_k x q_i)], fp16 -> TMEM ----
@@ -272,7 +296,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[D / 2];
 #pragma unroll
         for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
-        if (valid) row_operand_f16<D>(qrow, k2row, a.a_scale, p.det, pk);
+        if (valid) {
+          if (p.det) {
+            row_operand_from_f16<D>(qrow, k2row, a.a_scale, pk);
+          } else {  // unscaled q o k2 (the scale is applied by the softmax FFMA)
+            const uint4* xp = reinterpret_cast<const uint4*>(qrow);
+            const uint4* yp = reinterpret_cast<const uint4*>(k2row);
+#pragma unroll
+            for (int t = 0; t < D / 8; ++t) {
+              const uint4 xv = xp[t], yv = yp[t];
+              pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
+              pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
+              pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
+              pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
+            }
+          }
+        }
         SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 29 << 8);
         tmem_store_row<D>(tA, pk);
         tmem_st_wait();
@@ -307,17 +346,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           hi_c = 0;
         }
         const bool need_mask = lo_c > 0 || hi_c < 63;
-        float mx = -INFINITY;
-        if (!__any_sync(0xffffffffu, need_mask)) {
+        // row max as an 8-way tree (independent chains, not one 64-long dependency)
+        if (__any_sync(0xffffffffu, need_mask)) {
 #pragma unroll
-          for (int jj = 0; jj < 64; ++jj) mx = fmaxf(mx, sv[jj]);
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 64; ++jj) {
-            sv[jj] = (jj >= lo_c && jj <= hi_c) ? sv[jj] : -INFINITY;
-            mx = fmaxf(mx, sv[jj]);
-          }
+          for (int jj = 0; jj < 64; ++jj) sv[jj] = (jj >= lo_c && jj <= hi_c) ? sv[jj] : -INFINITY;
         }
+        float mx;
+        {
+          float m8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m8[u] = fmaxf(fmaxf(sv[u], sv[u + 8]), fmaxf(sv[u + 16], sv[u + 24]));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(fmaxf(sv[u + 32], sv[u + 40]), fmaxf(sv[u + 48], sv[u + 56])));
+          mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        }
+        mx *= a.sm_mult;  // sm_mult > 0: the max of the scaled logits
         if (c == 0) {
           m_ref = mx;
         } else {
@@ -343,13 +386,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
         uint32_t pk[32];
-        float ls = 0.f;
+        const float2 vmul = make_float2(a.sm_mult, a.sm_mult), vm = make_float2(-m_use, -m_use);
+        float2 ls4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          const float p0 = ex2(sv[2 * t] - m_use), p1 = ex2(sv[2 * t + 1] - m_use);
-          ls += p0 + p1;
-          pk[t] = pack_f16x2(p0, p1);
+          const float2 xx = ffma2(make_float2(sv[2 * t], sv[2 * t + 1]), vmul, vm);
+          const float2 pv = (t & 3) == 3 ? ex2_poly2(xx) : make_float2(ex2(xx.x), ex2(xx.y));
+          ls4[t & 3] = fadd2(ls4[t & 3], pv);  // 4 independent packed partial sums
+          pk[t] = pack_f16x2(pv);
         }
+        const float ls = ((ls4[0].x + ls4[0].y) + (ls4[1].x + ls4[1].y)) + ((ls4[2].x + ls4[2].y) + (ls4[3].x + ls4[3].y));
         l += ls;  // columns >= w were masked to -inf above (need_mask holds whenever w < 64)
         SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 24 << 8 | c);
         if (w == 64) tmem_st32(tS, pk);
@@ -516,8 +562,8 @@ bool tc_fwd_supported(const Problem& p) {
 }
 
 size_t tc_fwd_workspace_bytes(const Problem& p) {
-  size_t n = size_t(p.B) * p.NK() * p.H * p.D;
-  return 2 * ((n * 2 + 255) & ~size_t(255));
+  const size_t n = size_t(p.B) * p.NK() * p.H * p.D, nq = size_t(p.B) * p.N * p.H * p.D;
+  return 3 * ((n * 2 + 255) & ~size_t(255)) + ((nq * 2 + 255) & ~size_t(255));
 }
 
 cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const void* k, const void* v,
@@ -530,9 +576,13 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
     if (p.det) p.scale = -p.scale;
   }
   const size_t n = size_t(p.B) * p.NK() * p.H * p.D;
+  const size_t nq = size_t(p.B) * p.N * p.H * p.D;
   char* kf = (char*)ws;
   char* vf = kf + ((n * 2 + 255) & ~size_t(255));
+  char* k2f = vf + ((n * 2 + 255) & ~size_t(255));
+  char* qf = k2f + ((n * 2 + 255) & ~size_t(255));
   cudaError_t e = convert_pair_f16(k, kf, v, vf, int64_t(n), num_sms(), st);
+  if (e == cudaSuccess) e = convert_two_f16(q, qf, int64_t(nq), k2, k2f, int64_t(n), num_sms(), st);
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmV;
   if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.H, p.D, kChunk) ||
@@ -540,8 +590,8 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
     return cudaErrorInvalidValue;
   FwdArgs a;
   a.p = p;
-  a.q = (const __nv_bfloat16*)q;
-  a.k2 = (const __nv_bfloat16*)k2;
+  a.q = (const __half*)qf;
+  a.k2 = (const __half*)k2f;
   a.v2 = (const __nv_bfloat16*)v2;
   a.o = o;
   a.lse = lse;
@@ -552,6 +602,7 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
   a.npairs = (a.ngroups + 1) / 2;
   a.items = a.npairs * p.B * p.H;
   a.a_scale = p.scale * kLog2e;
+  a.sm_mult = p.det ? 1.f : p.scale * kLog2e;
   const int grid = std::min(a.items, num_sms());
   const bool staged = 2 * a.G + 2 * (a.R + 2 * a.G - 1) <= kStgRows;
   auto launch = [&](auto kern, size_t smem) {

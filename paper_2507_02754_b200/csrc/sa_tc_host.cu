@@ -37,11 +37,11 @@ bool make_tmap_bnhd_f16(CUtensorMap* m, const void* base, int B, int rows, int H
 namespace {
 // bf16 -> fp16, 8 elements per thread-iteration.  Exact for |x| in the fp16 normal range; the
 // MMA operands must share one 16-bit format.
-__global__ void __launch_bounds__(256) cvt_bf16_f16(const uint4* __restrict__ a, uint4* __restrict__ ao,
-                                                    const uint4* __restrict__ b, uint4* __restrict__ bo, int64_t n8) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < 2 * n8; t += int64_t(gridDim.x) * blockDim.x) {
-    const uint4* src = t < n8 ? a + t : b + (t - n8);
-    uint4* dst = t < n8 ? ao + t : bo + (t - n8);
+__global__ void __launch_bounds__(256) cvt_bf16_f16(const uint4* __restrict__ a, uint4* __restrict__ ao, int64_t na8,
+                                                    const uint4* __restrict__ b, uint4* __restrict__ bo, int64_t nb8) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < na8 + nb8; t += int64_t(gridDim.x) * blockDim.x) {
+    const uint4* src = t < na8 ? a + t : b + (t - na8);
+    uint4* dst = t < na8 ? ao + t : bo + (t - na8);
     uint4 x = __ldg(src);
     uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -52,18 +52,24 @@ __global__ void __launch_bounds__(256) cvt_bf16_f16(const uint4* __restrict__ a,
     *dst = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
+
 }  // namespace
 
-// Convert two bf16 tensors of n elements each (n % 8 == 0) into fp16 copies.
-cudaError_t convert_pair_f16(const void* a, void* ao, const void* b, void* bo, int64_t n, int num_sms,
-                             cudaStream_t st) {
-  int64_t n8 = n / 8;
-  int blocks = int((2 * n8 + 255) / 256);
+// bf16 -> fp16 copies of two tensors of na and nb elements (multiples of 8), one launch.
+cudaError_t convert_two_f16(const void* a, void* ao, int64_t na, const void* b, void* bo, int64_t nb, int num_sms,
+                            cudaStream_t st) {
+  const int64_t na8 = na / 8, nb8 = nb / 8;
+  int blocks = int((na8 + nb8 + 255) / 256);
   if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (blocks < 1) blocks = 1;
   KernelScope ks("tc_cvt_f16", st);
-  cvt_bf16_f16<<<blocks, 256, 0, st>>>((const uint4*)a, (uint4*)ao, (const uint4*)b, (uint4*)bo, n8);
+  cvt_bf16_f16<<<blocks, 256, 0, st>>>((const uint4*)a, (uint4*)ao, na8, (const uint4*)b, (uint4*)bo, nb8);
   return cudaGetLastError();
+}
+
+cudaError_t convert_pair_f16(const void* a, void* ao, const void* b, void* bo, int64_t n, int num_sms,
+                             cudaStream_t st) {
+  return convert_two_f16(a, ao, n, b, bo, n, num_sms, st);
 }
 
 int num_sms() {

@@ -68,6 +68,56 @@ __device__ __forceinline__ void row_operand_f16(const __nv_bfloat16* x, const __
   }
 }
 
+__device__ __forceinline__ uint32_t hmul2_u32(uint32_t x, uint32_t y) {
+  __half2 r = __hmul2(*reinterpret_cast<__half2*>(&x), *reinterpret_cast<__half2*>(&y));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// Determinant row operand from fp16 rows: scale * (y x x) chunkwise, trailing D mod 3 dims 0.
+template <int D>
+__device__ __forceinline__ void row_operand_from_f16(const __half* x, const __half* y, float scale,
+                                                     uint32_t (&pk)[D / 2]) {
+  const uint4* xp = reinterpret_cast<const uint4*>(x);
+  const uint4* yp = reinterpret_cast<const uint4*>(y);
+  constexpr int D3 = (D / 3) * 3;
+#pragma unroll
+  for (int base = 0; base < D; base += 24) {
+    float xf[24], yf[24], av[24];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      if (base + 8 * u < D) {
+        uint4 a = xp[base / 8 + u], b = yp[base / 8 + u];
+        uint32_t as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 fa = __half22float2(*reinterpret_cast<__half2*>(&as[e]));
+          float2 fb = __half22float2(*reinterpret_cast<__half2*>(&bs[e]));
+          xf[8 * u + 2 * e] = fa.x;
+          xf[8 * u + 2 * e + 1] = fa.y;
+          yf[8 * u + 2 * e] = fb.x;
+          yf[8 * u + 2 * e + 1] = fb.y;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int c3 = 0; c3 < 24; c3 += 3) {
+      if (base + c3 + 3 <= D3) {  // (y x x)_r = y_{r+1} x_{r+2} - y_{r+2} x_{r+1}
+        av[c3 + 0] = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+        av[c3 + 1] = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+        av[c3 + 2] = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+      } else {
+        av[c3 + 0] = av[c3 + 1] = av[c3 + 2] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 24; e += 2)
+      if (base + e < D) pk[(base + e) / 2] = pack_f16x2(scale * av[e], scale * av[e + 1]);
+  }
+}
+
 // Store a full packed row (D/2 columns) to TMEM at column address taddr (this warp's lanes).
 template <int D>
 __device__ __forceinline__ void tmem_store_row(uint32_t taddr, const uint32_t (&pk)[D / 2]) {
