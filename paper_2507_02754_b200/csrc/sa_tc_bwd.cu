@@ -60,8 +60,13 @@ __global__ void __launch_bounds__(256) delta_kernel(Problem p, const __nv_bfloat
 // ==========================================================================================
 // bwd_q: dQ, dK2, dV2
 // ==========================================================================================
-constexpr int kQThreads = 320;
-constexpr int kQWarpTMA = 8, kQWarpMMA = 9;  // compute warps 0-7 (see tc_fwd: high ids win issue)
+// 16 compute warps: warp w -> TMEM lane quarter w&3, column half (w>>2)&1, sub-slice w>>3 (two warps
+// per lane quarter and half: more warps in flight to hide the latency of the softmax-gradient, the
+// row-operand formation and the epilogue)
+constexpr int kQCW = 16;
+constexpr int kQNT = 32 * kQCW;  // compute threads
+constexpr int kQThreads = kQNT + 64;
+constexpr int kQWarpTMA = kQCW, kQWarpMMA = kQCW + 1;
 constexpr int kQChunk = 64;
 // TMEM columns
 constexpr uint32_t kQW = 0, kQU = 128, kQS = 256, kQdP = 320, kQAS = 384, kQAdP = 448;
@@ -149,10 +154,11 @@ struct QRows {
 template <int D, int RING, bool STAGED, int PW, bool DET>
 __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
                                                 int c0, int half, int r, bool valid, const QRows& rw, uint32_t tW,
-                                                uint32_t tU, int tid256) {
+                                                uint32_t tU, int tid256, bool p1) {
   const Problem& p = a.p;
   const float s = p.scale;
-  if (half == 0) {
+  if (!p1) {
+  } else if (half == 0) {
     float wv[PW], k2v[PW], qv[PW];
     {
       uint32_t u[PW];
@@ -242,10 +248,10 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
 #pragma unroll
     for (int e = 0; e < PW; ++e) sm.eb.g.ev[r][e] = dov[e] * uv[e];
   }
-  named_bar_sync(1, 256);
+  named_bar_sync(1, kQNT);
   // dq: sum over the R rows of each query; 4 lanes per output, rows interleaved, shuffle-combined
   const bool dq_done = !DET && PW == 16 && a.R == 32;
-  for (int base = 0; !dq_done && base < it.nq * PW * 4; base += 256) {
+  for (int base = 0; !dq_done && base < it.nq * PW * 4; base += kQNT) {
     const int idx = base + tid256;
     const bool act = idx < it.nq * PW * 4;
     const int o = idx >> 2, part = idx & 3;
@@ -275,7 +281,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
   const int sbase = (P0 - a.R + 1 + a.ring) % a.ring;
-  for (int idx = tid256; idx < nsl * PW; idx += 256) {
+  for (int idx = tid256; idx < nsl * PW; idx += kQNT) {
     const int sl = idx / PW, d = idx % PW;
     const int kp = P0 - a.R + 1 + sl;
     if (kp < 0) continue;
@@ -298,38 +304,40 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     sm.acc_k2[slot][c0 + d] += xk;
     sm.acc_v2[slot][c0 + d] += xv;
   }
-  named_bar_sync(1, 256);
+  named_bar_sync(1, kQNT);
 }
 
-// R = 32 trilinear pass over 32 columns: the warp of query g holds its 32 rows, so dq is a register
-// reduce-scatter (lane L ends with column c0+L); dk2/dv2 go through the shared-memory gather.
+// R = 32 trilinear pass over 32 columns [c0, c0+32): sub-warp `sub` takes columns c0+16 sub .. +16.
+// The warp of query g holds its 32 rows, so dq is a register reduce-scatter (lane pairs end with one
+// column); dk2/dv2 go through the shared-memory gather over all compute threads.
 template <int D, int RING, bool STAGED>
 __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
-                                                  int c0, int half, int r, bool valid, const QRows& rw, uint32_t tW,
-                                                  uint32_t tU, int tid256) {
+                                                  int c0, int half, int sub, int r, bool valid, const QRows& rw,
+                                                  uint32_t tW, uint32_t tU, int tidc, int sbase) {
   const Problem& p = a.p;
   const float s = p.scale;
   const int ln = r & 31;
+  const int cs = c0 + 16 * sub;
   if (half == 0) {
-    uint32_t u[32];
-    tmem_ld32(tW + c0, u);
+    uint32_t u[16];
+    tmem_ld16(tW + cs, u);
     tmem_ld_wait();
-    float k2v[32], qv[32], v[32];
+    float k2v[16], qv[16], v[16];
     if (valid) {
-      load_f16<32>(rw.k2 + c0, k2v);
-      load_f16<32>(rw.q + c0, qv);
+      load_f16<16>(rw.k2 + cs, k2v);
+      load_f16<16>(rw.q + cs, qv);
     } else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) k2v[e] = qv[e] = 0.f;
+      for (int e = 0; e < 16; ++e) k2v[e] = qv[e] = 0.f;
     }
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
+    for (int e = 0; e < 16; ++e) {
       const float w = __uint_as_float(u[e]);
       v[e] = s * k2v[e] * w;
-      sm.eb.w.ek[r][e] = s * qv[e] * w;
+      sm.eb.w.ek[r][16 * sub + e] = s * qv[e] * w;
     }
 #pragma unroll
-    for (int st = 16, n = 16; st >= 1; st >>= 1, n >>= 1) {
+    for (int st = 16, n = 8; st >= 2; st >>= 1, n >>= 1) {
       const bool hi = ln & st;
 #pragma unroll
       for (int i = 0; i < n; ++i) {
@@ -337,36 +345,36 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
       }
     }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
     const int gq = r >> 5;
-    if (gq < it.nq) {
-      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + c0 + ln;
+    if ((ln & 1) == 0 && gq < it.nq) {
+      const int col = ((ln >> 4) & 1) * 8 + ((ln >> 3) & 1) * 4 + ((ln >> 2) & 1) * 2 + ((ln >> 1) & 1);
+      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + col;
       if (a.out_f32)
         reinterpret_cast<float*>(a.dq)[off] = v[0];
       else
         reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
     }
   } else {
-    uint32_t u[32];
-    tmem_ld32(tU + c0, u);
+    uint32_t u[16];
+    tmem_ld16(tU + cs, u);
     tmem_ld_wait();
-    float dov[32];
+    float dov[16];
     if (valid) {
-      load_f16<32>(rw.dO + c0, dov);
+      load_f16<16>(rw.dO + cs, dov);
     } else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) dov[e] = 0.f;
+      for (int e = 0; e < 16; ++e) dov[e] = 0.f;
     }
 #pragma unroll
-    for (int e = 0; e < 32; ++e) sm.eb.w.ev[r][e] = dov[e] * __uint_as_float(u[e]);
+    for (int e = 0; e < 16; ++e) sm.eb.w.ev[r][16 * sub + e] = dov[e] * __uint_as_float(u[e]);
   }
-  named_bar_sync(1, 256);
+  named_bar_sync(1, kQNT);
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
-  const int sbase = (P0 - a.R + 1 + a.ring) % a.ring;
-  for (int idx = tid256; idx < nsl * 32; idx += 256) {
+  for (int idx = tidc; idx < nsl * 32; idx += kQNT) {
     const int sl = idx >> 5, d = idx & 31;
     const int kp = P0 - a.R + 1 + sl;
-    if (kp < 0) continue;
     const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
     float tk[4], tv[4];
 #pragma unroll
@@ -378,10 +386,12 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
     }
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
-    sm.acc_k2[slot][c0 + d] += (tk[0] + tk[1]) + (tk[2] + tk[3]);
-    sm.acc_v2[slot][c0 + d] += (tv[0] + tv[1]) + (tv[2] + tv[3]);
+    if (kp >= 0) {
+      sm.acc_k2[slot][c0 + d] += (tk[0] + tk[1]) + (tk[2] + tk[3]);
+      sm.acc_v2[slot][c0 + d] += (tv[0] + tv[1]) + (tv[2] + tv[3]);
+    }
   }
-  named_bar_sync(1, 256);
+  named_bar_sync(1, kQNT);
 }
 
 template <int D, bool DET, int RING, bool STAGED>
@@ -408,10 +418,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.sfull[s], 1);
-      mbar_init(&sm.pready[s], 4);
+      mbar_init(&sm.pready[s], 8);
     }
     mbar_init(&sm.udone, 1);
-    mbar_init(&sm.aready, 8);
+    mbar_init(&sm.aready, kQCW);
     fence_mbar_init();
   }
   if (warp == kQWarpMMA) tmem_alloc<512>(&sm.tmem_base);
@@ -497,7 +507,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
             for (int k2i = 0; k2i < nwh / 16; ++k2i) {
               const uint32_t acc = (c > 0 || hh > 0 || k2i > 0) ? 1u : 0u;
               const uint32_t roff = (32 * hh + 16 * k2i) * 128;
-              const uint32_t pc = 32 * hh + 8 * k2i;
+              const uint32_t pc = 32 * hh + 16 * k2i;  // packed P/dS of columns 32hh+16k2i.. (see the softmax)
               mma_ts_w(tW, tdP + pc, smem_desc_sw128(kaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
               mma_ts_w(tU, tS + pc, smem_desc_sw128(vaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
             }
@@ -516,11 +526,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
         ++gc;
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < kQCW) {
     // ------------------------------ softmax-gradient + epilogue ------------------------------
-    const int qd = warp & 3, half = warp >> 2;
+    const int qd = warp & 3, half = (warp >> 2) & 1, sub = warp >> 3;
     const int r = qd * 32 + lane;
-    const int tid256 = threadIdx.x;
+    const int tid256 = threadIdx.x;  // 0 .. kQNT-1
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t tW = tbase + kQW + lane_off, tU = tbase + kQU + lane_off;
     const uint32_t tS = tbase + kQS + lane_off, tdP = tbase + kQdP + lane_off;
@@ -534,7 +544,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int P0 = p.np + it.i0;
       const int nk = a.R + a.G - 1;
       const int nrows = 2 * a.G + 2 * nk;
-      for (int task = tid256; task < nrows * kC8; task += 256) {
+      for (int task = tid256; task < nrows * kC8; task += kQNT) {
         const int row = task / kC8, c8 = task % kC8;
         const __half* src = nullptr;
         if (row < a.G) {
@@ -564,7 +574,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     if (it_begin < it_end) stage(it_begin, 0);
     for (int item = it_begin; item < it_end; ++item) {
       QItem it = q_item(a, item);
-      const bool tr = (threadIdx.x & 127) == 0 && item - it_begin >= 100 && item - it_begin < 102;
+      const bool tr = (threadIdx.x & 127) == 0 && threadIdx.x < 256 && item - it_begin >= 100 && item - it_begin < 102;
       const int treg = 1 + half;
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 1 << 8);
       const int buf = STAGED ? int(gc & 1) : 0;
@@ -575,7 +585,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         } else {
           cp_async_wait<0>();
         }
-        named_bar_sync(1, 256);
+        named_bar_sync(1, kQNT);
       }
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 8 << 8);
       const bool first_in_sub = item == it_begin || it.grp == 0;
@@ -617,14 +627,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
       }
       // ---- row operands (fp16, unscaled): half 0 -> A_S = q o k2 [det: k2 x q], half 1 -> A_dP = dO o v2 ----
-      {
+      if (DET && half == 0) {
         uint32_t pk[D / 2];
 #pragma unroll
         for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
-        if (valid) {
-          const __half* x = half == 0 ? rw.q : rw.dO;
-          const __half* y = half == 0 ? rw.k2 : rw.v2;
-          if (DET && half == 0) {
+        if (valid && sub == 0) {
+          const __half* x = rw.q;
+          const __half* y = rw.k2;
+          {
             constexpr int D3 = (D / 3) * 3;
 #pragma unroll
             for (int base = 0; base < D; base += 24) {
@@ -661,20 +671,38 @@ __global__ void __launch_bounds__(kQThreads, 1)
               for (int e = 0; e < 24; e += 2)
                 if (base + e < D) pk[(base + e) / 2] = pack_f16x2(xf[e], xf[e + 1]);
             }
-          } else {
+          }
+        }
+        if (sub == 0) tmem_store_row<D>(tAS, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.aready);
+      } else {
+        // trilinear (A_S = q o k2) or A_dP = dO o v2: sub-warp `sub` forms columns [D/2 sub, D/2 sub + D/2)
+        constexpr int DH = D / 2;
+        uint32_t pk[DH / 2];
 #pragma unroll
-            for (int t = 0; t < D / 8; ++t) {
-              const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * t);
-              const uint4 yv = *reinterpret_cast<const uint4*>(y + 8 * t);
-              pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
-              pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
-              pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
-              pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
-            }
+        for (int t = 0; t < DH / 2; ++t) pk[t] = 0u;
+        if (valid) {
+          const __half* x = (half == 0 ? rw.q : rw.dO) + DH * sub;
+          const __half* y = (half == 0 ? rw.k2 : rw.v2) + DH * sub;
+#pragma unroll
+          for (int t = 0; t < DH / 8; ++t) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * t);
+            const uint4 yv = *reinterpret_cast<const uint4*>(y + 8 * t);
+            pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
+            pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
+            pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
+            pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
           }
         }
         SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 9 << 8);
-        tmem_store_row<D>(half == 0 ? tAS : tAdP, pk);
+        const uint32_t ta = (half == 0 ? tAS : tAdP) + (DH / 2) * sub;
+        if constexpr (DH == 64)
+          tmem_st32(ta, pk);
+        else
+          tmem_st16(ta, pk);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -685,20 +713,15 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int jlo = max(0, pos - p.w1 + 1);
       for (int c = 0; c < it.nch; ++c) {
         const int w = q_width(it, c);
-        const int cb = 32 * half;
-        const int nw = max(0, min(32, w - cb));
+        const int cb = 32 * half + 16 * sub;  // this warp's 16 columns of the 64-column chunk
+        const int nw = max(0, min(16, w - cb));
         mbar_wait(&sm.sfull[half], (kc + c) & 1);
         tc_fence_after();
         SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 3 << 8 | c);
-        if (nw > 0) {
-          uint32_t su[32], du[32];
-          if (nw == 32) {
-            tmem_ld32(tS + cb, su);
-            tmem_ld32(tdP + cb, du);
-          } else {
-            tmem_ld16(tS + cb, su);
-            tmem_ld16(tdP + cb, du);
-          }
+        if (nw > 0) {  // chunk widths are multiples of 16: nw is 0 or 16 (warp-uniform)
+          uint32_t su[16], du[16];
+          tmem_ld16(tS + cb, su);
+          tmem_ld16(tdP + cb, du);
           tmem_ld_wait();
           const int jc0 = it.jbeg + c * kQChunk + cb;
           int lo_c = jlo - jc0, hi_c = min(pos - jc0, nw - 1);
@@ -706,12 +729,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
             lo_c = 1;
             hi_c = 0;
           }
-          const bool need_mask = lo_c > 0 || hi_c < 31;
-          uint32_t pp[16], pd[16];
+          const bool need_mask = lo_c > 0 || hi_c < 15;
+          uint32_t pp[8], pd[8];
           if (!__any_sync(0xffffffffu, need_mask)) {
             const float2 vs = make_float2(sl2, sl2), vl = make_float2(-lse_l2, -lse_l2), vd = make_float2(-dl, -dl);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
+            for (int t = 0; t < 8; ++t) {
               const float2 x = ffma2(make_float2(__uint_as_float(su[2 * t]), __uint_as_float(su[2 * t + 1])), vs, vl);
               const float2 pv = make_float2(ex2(x.x), ex2(x.y));
               pp[t] = pack_f16x2(pv);
@@ -720,7 +743,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
+            for (int t = 0; t < 8; ++t) {
               float p0 = ex2(fmaf(__uint_as_float(su[2 * t]), sl2, -lse_l2));
               float p1 = ex2(fmaf(__uint_as_float(su[2 * t + 1]), sl2, -lse_l2));
               p0 = (2 * t >= lo_c && 2 * t <= hi_c) ? p0 : 0.f;
@@ -729,13 +752,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
               pd[t] = pack_f16x2(p0 * (__uint_as_float(du[2 * t]) - dl), p1 * (__uint_as_float(du[2 * t + 1]) - dl));
             }
           }
-          if (nw == 32) {
-            tmem_st16(tS + cb, pp);
-            tmem_st16(tdP + cb, pd);
-          } else {
-            tmem_st8(tS + cb, pp);
-            tmem_st8(tdP + cb, pd);
-          }
+          // P / dS of columns [cb, cb+16) overwrite the first 8 columns of this warp's own S / dP
+          // range (the other sub-warp may still be reading its range)
+          tmem_st8(tS + cb, pp);
+          tmem_st8(tdP + cb, pd);
           tmem_st_wait();
         }
         tc_fence_before();
@@ -750,19 +770,21 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (DET) {
 #pragma unroll 1
         for (int c0 = 0; c0 + 24 <= D; c0 += 24)
-          q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
+          q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256, sub == 0);
         if constexpr (D % 24 != 0)
-          q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256);
+          q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256,
+                                                        sub == 0);
       } else if (a.R == 32) {
 #pragma unroll 1
+        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
         for (int c0 = 0; c0 < D; c0 += 32) {
-          q_epilogue_pass32<D, RING, STAGED>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
+          q_epilogue_pass32<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
           SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | (c0 / 32));
         }
       } else {
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 16)
-          q_epilogue_pass<D, RING, STAGED, 16, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256);
+          q_epilogue_pass<D, RING, STAGED, 16, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256, sub == 0);
       }
       tc_fence_before();
       // ---- flush ring rows that no later tile of this sub-range touches ----
@@ -772,7 +794,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool start_open = PS > p.np;
       const int nrows = flush_hi - flush_lo + 1;
       const int fbase = (flush_lo + a.ring) % a.ring;
-      for (int idx = tid256; idx < nrows * D; idx += 256) {
+      for (int idx = tid256; idx < nrows * D; idx += kQNT) {
         const int kp = flush_lo + idx / D, d = idx % D;
         if (kp < 0 || kp >= p.NK()) continue;
         int slot = fbase + idx / D;
@@ -802,7 +824,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
       }
       flush_lo = flush_hi + 1;
-      named_bar_sync(1, 256);
+      named_bar_sync(1, kQNT);
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 7 << 8);
       kc += it.nch;
       ++gc;
