@@ -116,9 +116,14 @@ sa_status simplicial_attn_bwd_prefixed(const void* q, const void* k, const void*
                                        int64_t w2, int64_t n_prefix, uint32_t flags, void* stream);
 
 /* End-to-end step from HOST buffers: copies the six inputs host->device into the caller's device
- * scratch, runs forward and backward, and copies o, lse and the five gradients device->host, all
- * on `stream` (pinned host memory makes the copies asynchronous).  Host layouts/dtypes as above
- * (n_prefix = 0).  d_scratch must hold simplicial_attn_host_step_scratch_bytes(...) bytes. */
+ * scratch, runs forward and backward, and copies o, lse and the five gradients device->host.
+ * Host layouts/dtypes as above (n_prefix = 0).  d_scratch must hold
+ * simplicial_attn_host_step_scratch_bytes(...) bytes.  With B > 1 the step is pipelined per batch
+ * element (every (b,h) slice is independent): the copies of slice b+1 in and b-1 out run on
+ * two library-owned copy streams while slice b computes on `stream`.  Ordering is still that of
+ * `stream`: the copies start after the work already queued on it, and `stream` waits for the last
+ * device->host copy, so the results are valid once the caller syncs `stream`.  Host buffers must be
+ * pinned for the copies to overlap (pageable memory works but serialises). */
 size_t simplicial_attn_host_step_scratch_bytes(int64_t B, int64_t H, int64_t N, int64_t D,
                                                int64_t w1, int64_t w2, uint32_t flags);
 sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void* h_v,

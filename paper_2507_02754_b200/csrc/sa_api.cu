@@ -221,6 +221,36 @@ sa_status simplicial_attn_bwd(const void* q, const void* k, const void* v, const
 }
 
 // Device scratch layout of the host step: 6 inputs | o | lse | 5 grads | bwd workspace.
+// Copy streams and events of the pipelined host step (one set per device, created on first use).
+struct HostPipe {
+  bool ok = false;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t entry = nullptr, out = nullptr;
+  std::vector<cudaEvent_t> in, done;
+};
+static HostPipe& host_pipe(int nchunks) {
+  static std::mutex mu;
+  static HostPipe pipes[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  HostPipe& hp = pipes[dev & 63];
+  if (!hp.h2d) {
+    hp.ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&hp.entry, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&hp.out, cudaEventDisableTiming) == cudaSuccess;
+  }
+  while (hp.ok && int(hp.in.size()) < nchunks) {
+    cudaEvent_t a, b;
+    hp.ok = cudaEventCreateWithFlags(&a, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&b, cudaEventDisableTiming) == cudaSuccess;
+    hp.in.push_back(a);
+    hp.done.push_back(b);
+  }
+  return hp;
+}
+
 static size_t host_step_layout(const Problem& p, uint32_t flags, size_t off[16]) {
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   size_t ein = in_f32 ? 4 : 2, eout = out_f32 ? 4 : 2;
@@ -260,28 +290,42 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
   size_t need = host_step_layout(p, flags, off);
   if (scratch_bytes < need) return SA_ERR_WORKSPACE;
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
-  size_t nel = size_t(p.B) * p.N * p.H * p.D;
-  size_t bin = nel * (in_f32 ? 4 : 2), bout = nel * (out_f32 ? 4 : 2);
-  size_t blse = sizeof(float) * size_t(p.B) * p.H * p.N;
+  const size_t nel = size_t(p.B) * p.N * p.H * p.D;
+  const int64_t nb = B;  // pipeline chunks: batch elements (contiguous slices of every tensor)
+  const size_t sin = nel / nb * (in_f32 ? 4 : 2), sout = nel / nb * (out_f32 ? 4 : 2);
+  const size_t slse = sizeof(float) * size_t(p.H) * p.N;
   char* base = (char*)d_scratch;
   cudaStream_t st = (cudaStream_t)stream;
   cudaGetLastError();
-  for (int t = 0; t < 6; ++t) {
-    cudaError_t e = cudaMemcpyAsync(base + off[t], hin[t], bin, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_status(e);
+  HostPipe& hp = host_pipe(int(nb));
+  if (!hp.ok) return SA_ERR_CUDA;
+  cudaError_t e = cudaEventRecord(hp.entry, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.h2d, hp.entry, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.entry, 0);
+  for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
+    for (int t = 0; t < 6 && e == cudaSuccess; ++t)
+      e = cudaMemcpyAsync(base + off[t] + b * sin, (const char*)hin[t] + b * sin, sin, cudaMemcpyHostToDevice,
+                          hp.h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(hp.in[b], hp.h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.in[b], 0);
+    if (e != cudaSuccess) break;
+    auto P = [&](int t) { return base + off[t] + b * (t < 6 ? sin : sout); };
+    float* lse_b = (float*)(base + off[7]) + b * p.H * p.N;
+    s = simplicial_attn_fwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_b, 1, H, N, D, w1, w2, flags, stream);
+    if (s != SA_OK) return s;
+    s = simplicial_attn_bwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_b, P(5), P(8), P(9), P(10), P(11), P(12),
+                            base + off[13], off[14] - off[13], 1, H, N, D, w1, w2, flags, stream);
+    if (s != SA_OK) return s;
+    e = cudaEventRecord(hp.done[b], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.done[b], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)h_o + b * sout, P(6), sout, cudaMemcpyDeviceToHost, hp.d2h);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((char*)h_lse + b * slse, lse_b, slse, cudaMemcpyDeviceToHost, hp.d2h);
+    for (int t = 0; t < 5 && e == cudaSuccess; ++t)
+      e = cudaMemcpyAsync((char*)hout[t] + b * sout, P(8 + t), sout, cudaMemcpyDeviceToHost, hp.d2h);
   }
-  s = simplicial_attn_fwd(base + off[0], base + off[1], base + off[2], base + off[3], base + off[4],
-                          base + off[6], (float*)(base + off[7]), B, H, N, D, w1, w2, flags, stream);
-  if (s != SA_OK) return s;
-  s = simplicial_attn_bwd(base + off[0], base + off[1], base + off[2], base + off[3], base + off[4],
-                          base + off[6], (const float*)(base + off[7]), base + off[5], base + off[8],
-                          base + off[9], base + off[10], base + off[11], base + off[12], base + off[13],
-                          off[14] - off[13], B, H, N, D, w1, w2, flags, stream);
-  if (s != SA_OK) return s;
-  cudaError_t e = cudaMemcpyAsync(h_o, base + off[6], bout, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h_lse, base + off[7], blse, cudaMemcpyDeviceToHost, st);
-  for (int t = 0; t < 5 && e == cudaSuccess; ++t)
-    e = cudaMemcpyAsync(hout[t], base + off[8 + t], bout, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaEventRecord(hp.out, hp.d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.out, 0);
   return cuda_status(e);
 }
 

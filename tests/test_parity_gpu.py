@@ -124,8 +124,12 @@ def test_deterministic():
         assert torch.equal(a[n], b[n]), n
 
 
-def test_host_step_matches_device_path():
-    B, N, H, D, w1, w2 = 1, 256, 2, 128, 64, 32
+@pytest.mark.parametrize("B", [1, 3])
+def test_host_step_matches_device_path(B):
+    """The end-to-end host step (pipelined per batch element when B > 1) reproduces the device
+    path: bitwise where the per-slice decomposition is the same (o, lse, dq, dk, dv); dk2/dv2 may
+    differ in fp32 summation order because the per-CTA tile ranges of bwd_q depend on B."""
+    N, H, D, w1, w2 = 256, 2, 128, 64, 32
     inp = make_inputs(B, N, H, D, seed=17, dtype="bf16")
     dev = run_cuda(inp, w1, w2, False)
     h_in = {n: x.pin_memory() for n, x in inp.items()}
@@ -133,7 +137,10 @@ def test_host_step_matches_device_path():
     sa.host_step(h_in, h_out, w1, w2, out_f32=True)
     torch.cuda.synchronize()
     for n in dev:
-        assert torch.equal(h_out[n], dev[n].cpu()), n
+        if n in ("dk2", "dv2"):
+            assert torch.allclose(h_out[n], dev[n].cpu(), rtol=0, atol=1e-4), n
+        else:
+            assert torch.equal(h_out[n], dev[n].cpu()), n
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
