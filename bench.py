@@ -78,6 +78,19 @@ def kernel_work(name: str, c: dict, out_bytes: int):
     return table.get(name)
 
 
+def kernel_traffic(name: str, c: dict):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of `name` from the
+    newest committed `ncu --set full` summary for this config (profiles/*_traffic_<cfg>.json,
+    written by tools/profile_summarize.py), or (None, reason)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_traffic_{c['name']}.json")), key=os.path.getmtime)
+    for fn in reversed(files):
+        k = json.load(open(fn)).get("kernels", {}).get(name)
+        if k:
+            return k["traffic_bytes"], f"profiles/{os.path.basename(fn)} (one ncu --set full capture)"
+    return None, "no ncu --set full capture committed for this config"
+
+
 def alu_peak_tflops(sm_mhz: float) -> float:
     """fp32 FMA peak: 148 SMs x 128 FP32 lanes x 2 flop x clock."""
     return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
@@ -346,8 +359,10 @@ def main():
             else:
                 ach, unit = amount / (avg_ms / 1e3) / 1e12, "TFLOP/s"
                 peak = alu_peak_tflops(clk.get("sm_max_mhz") or 1965.0)
+            traffic, traffic_src = kernel_traffic(dom, c)
             roof = {"bound": bound, "kernel": dom, "achieved": ach, "peak": peak, "unit": unit,
-                    "frac": ach / peak, "traffic": None, "avg_launch_ms": avg_ms, "launches": cnt,
+                    "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "algorithmic_per_launch": amount, "avg_launch_ms": avg_ms, "launches": cnt,
                     "share_of_step": step_share,
                     "peak_source": (f"{pk_src} MEASURED_PEAKS.json bf16_tflops_sustained" if bound == "tensor"
                                     else f"{pk_src} hbm_gbs" if bound == "hbm"
