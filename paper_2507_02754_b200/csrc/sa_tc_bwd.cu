@@ -307,9 +307,10 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
   named_bar_sync(1, kQNT);
 }
 
-// R = 32 trilinear pass over 32 columns [c0, c0+32): sub-warp `sub` takes columns c0+16 sub .. +16.
-// The warp of query g holds its 32 rows, so dq is a register reduce-scatter (lane pairs end with one
-// column); dk2/dv2 go through the shared-memory gather over all compute threads.
+// R = 32 trilinear pass over 32 columns [c0, c0+32): the four warps of a TMEM lane quarter (= one
+// query g, 32 rows) split the columns 8 ways each: warp m = 2 half + sub takes columns c0+8m..+8
+// of both W (dq and the dk2 rows) and U (the dv2 rows).  dq is a register reduce-scatter over the
+// 32 lanes (lane groups of 4 end with one column); dk2/dv2 go through the shared-memory gather.
 template <int D, int RING, bool STAGED>
 __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
                                                   int c0, int half, int sub, int r, bool valid, const QRows& rw,
@@ -317,61 +318,57 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
   const Problem& p = a.p;
   const float s = p.scale;
   const int ln = r & 31;
-  const int cs = c0 + 16 * sub;
-  if (half == 0) {
-    uint32_t u[16];
-    tmem_ld16(tW + cs, u);
-    tmem_ld_wait();
-    float k2v[16], qv[16], v[16];
-    if (valid) {
-      load_f16<16>(rw.k2 + cs, k2v);
-      load_f16<16>(rw.q + cs, qv);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) k2v[e] = qv[e] = 0.f;
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float w = __uint_as_float(u[e]);
-      v[e] = s * k2v[e] * w;
-      sm.eb.w.ek[r][16 * sub + e] = s * qv[e] * w;
-    }
-#pragma unroll
-    for (int st = 16, n = 8; st >= 2; st >>= 1, n >>= 1) {
-      const bool hi = ln & st;
-#pragma unroll
-      for (int i = 0; i < n; ++i) {
-        const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-      }
-    }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    const int gq = r >> 5;
-    if ((ln & 1) == 0 && gq < it.nq) {
-      const int col = ((ln >> 4) & 1) * 8 + ((ln >> 3) & 1) * 4 + ((ln >> 2) & 1) * 2 + ((ln >> 1) & 1);
-      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + col;
-      if (a.out_f32)
-        reinterpret_cast<float*>(a.dq)[off] = v[0];
-      else
-        reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
-    }
+  const int m = 2 * half + sub;
+  const int cs = c0 + 8 * m;
+  uint32_t uw[8], uu[8];
+  tmem_ld8(tW + cs, uw);
+  tmem_ld8(tU + cs, uu);
+  float k2v[8], qv[8], dov[8];
+  if (valid) {
+    load_f16<8>(rw.k2 + cs, k2v);
+    load_f16<8>(rw.q + cs, qv);
+    load_f16<8>(rw.dO + cs, dov);
   } else {
-    uint32_t u[16];
-    tmem_ld16(tU + cs, u);
-    tmem_ld_wait();
-    float dov[16];
-    if (valid) {
-      load_f16<16>(rw.dO + cs, dov);
-    } else {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) dov[e] = 0.f;
+    for (int e = 0; e < 8; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
+  }
+  tmem_ld_wait();
+  float v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float w = __uint_as_float(uw[e]);
+    v[e] = s * k2v[e] * w;
+    sm.eb.w.ek[r][8 * m + e] = s * qv[e] * w;
+    sm.eb.w.ev[r][8 * m + e] = dov[e] * __uint_as_float(uu[e]);
+  }
+  // reduce-scatter the 8 columns over the 32 lanes: after the xor-16/8/4 stages lane L holds column
+  // (L>>4)&1 | ((L>>3)&1)<<1 | ((L>>2)&1)<<2 summed over 8 lanes; xor 2 and 1 finish the sum
+#pragma unroll
+  for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+    const bool hi = ln & st;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
     }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) sm.eb.w.ev[r][16 * sub + e] = dov[e] * __uint_as_float(u[e]);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  const int gq = r >> 5;
+  if ((ln & 3) == 0 && gq < it.nq) {
+    const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+    const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + col;
+    if (a.out_f32)
+      reinterpret_cast<float*>(a.dq)[off] = v[0];
+    else
+      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
   }
   named_bar_sync(1, kQNT);
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
+#ifdef SA_ABLATE_GATHER
+  if (nsl > 0) return;
+#endif
   for (int idx = tidc; idx < nsl * 32; idx += kQNT) {
     const int sl = idx >> 5, d = idx & 31;
     const int kp = P0 - a.R + 1 + sl;

@@ -87,6 +87,7 @@ int main() {
   run<64, false, false>(d);
   run<128, false, false>(d);
   run<256, false, false>(d);
+  run<16, true, false>(d);
   run<32, true, false>(d);
   run<64, true, false>(d);
   run<128, true, false>(d);

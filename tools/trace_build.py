@@ -7,7 +7,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 objs = []
 for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
     obj = f"/tmp/trace_{os.path.basename(src)}.o"
-    subprocess.check_call(["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-rdc=true", "-DSA_TRACE",
+    subprocess.check_call(["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-rdc=true", "-DSA_TRACE", *os.environ.get("SA_EXTRA", "").split(),
                            "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-c", src, "-o", obj])
     objs.append(obj)
 subprocess.check_call(["nvcc", *ARCH, "-shared", "-rdc=true", "-o", OUT, *objs])
