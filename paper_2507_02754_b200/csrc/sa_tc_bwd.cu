@@ -472,18 +472,22 @@ __global__ void __launch_bounds__(kQThreads, 1)
           const int s = (kc + c) % kStages;
           const int w = q_width(it, c);
           const int nwh = min(32, w - 32 * hh);
-          if (nwh > 0) {
-            const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
-            const uint32_t idesc_s = idesc_f16(128, nwh, 0, 0);
+          // one elected thread issues the group: descriptors advance by 64-bit adds in uniform registers
+          const uint64_t dk = smem_desc_sw128(smem_u32(sm.k[s]) + hh * 32 * 128, 16, 1024);
+          const uint64_t dv = smem_desc_sw128(smem_u32(sm.v[s]) + hh * 32 * 128, 16, 1024);
+          const uint32_t idesc_s = idesc_f16(128, nwh > 0 ? nwh : 16, 0, 0);
+          if (elect_one()) {
+            if (nwh > 0) {
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + hh * 32 * 128;
-              mma_ts_w(tS + 32 * hh, tAS + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-              mma_ts_w(tdP + 32 * hh, tAdP + kk * 8, smem_desc_sw128(vaddr + off, 16, 1024), idesc_s,
-                       kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+                mma_ts(tS + 32 * hh, tAS + kk * 8, desc_adv(dk, off), idesc_s, kk > 0 ? 1u : 0u);
+                mma_ts(tdP + 32 * hh, tAdP + kk * 8, desc_adv(dv, off), idesc_s, kk > 0 ? 1u : 0u);
+              }
             }
+            mma_commit(&sm.sfull[hh]);
           }
-          mma_commit_w(&sm.sfull[hh]);
+          __syncwarp();
         };
         {
           mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
@@ -501,13 +505,17 @@ __global__ void __launch_bounds__(kQThreads, 1)
             tc_fence_after();
             SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | (11 + hh) << 8 | c);
             const int nwh = min(32, w - 32 * hh);
-            for (int k2i = 0; k2i < nwh / 16; ++k2i) {
-              const uint32_t acc = (c > 0 || hh > 0 || k2i > 0) ? 1u : 0u;
-              const uint32_t roff = (32 * hh + 16 * k2i) * 128;
-              const uint32_t pc = 32 * hh + 16 * k2i;  // packed P/dS of columns 32hh+16k2i.. (see the softmax)
-              mma_ts_w(tW, tdP + pc, smem_desc_sw128(kaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
-              mma_ts_w(tU, tS + pc, smem_desc_sw128(vaddr + roff, kPanelBytes, 1024), idesc_acc, acc);
+            const uint64_t dk = smem_desc_sw128(kaddr, kPanelBytes, 1024), dv = smem_desc_sw128(vaddr, kPanelBytes, 1024);
+            if (elect_one()) {
+              for (int k2i = 0; k2i < nwh / 16; ++k2i) {
+                const uint32_t acc = (c > 0 || hh > 0 || k2i > 0) ? 1u : 0u;
+                const uint32_t roff = (32 * hh + 16 * k2i) * 128;
+                const uint32_t pc = 32 * hh + 16 * k2i;  // packed P/dS of columns 32hh+16k2i.. (see the softmax)
+                mma_ts(tW, tdP + pc, desc_adv(dk, roff), idesc_acc, acc);
+                mma_ts(tU, tS + pc, desc_adv(dv, roff), idesc_acc, acc);
+              }
             }
+            __syncwarp();
             if (c + 1 < it.nch) {
               if (hh == 0) {
                 mbar_wait(&sm.kvfull[(kc + c + 1) % kStages], ((kc + c + 1) / kStages) & 1);

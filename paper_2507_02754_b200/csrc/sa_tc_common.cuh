@@ -157,6 +157,10 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
   return d;
 }
 
+// Descriptor of the same tile advanced by `off` bytes (start-address field = addr >> 4; no carry
+// for shared addresses < 256 KB): one 64-bit add instead of rebuilding the descriptor per MMA.
+__device__ __forceinline__ uint64_t desc_adv(uint64_t d, uint32_t off) { return d + (off >> 4); }
+
 // D[tmem] (+)= A[tmem] * B[smem]   (A from TMEM, "TS" form), kind::f16, cta_group::1.
 __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                        uint32_t accumulate) {
