@@ -1304,14 +1304,18 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           tc_fence_after();
           SA_TRACE_AT(lane == 0 && t >= 50 && t < 53, 4, trn, t << 16 | 40 << 8);
         }
-        const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
+        const uint64_t da = smem_desc_sw128(smem_u32(sm.as[buf]) + q * 32 * 128, 16, 1024);
+        const uint64_t dd = smem_desc_sw128(smem_u32(sm.adp[buf]) + q * 32 * 128, 16, 1024);
+        if (elect_one()) {  // one thread issues the group (descriptors advance in uniform registers)
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32 + q * 32 * 128;
-          mma_ts_w(tSD + 64 * sb, tK + kk * 8, smem_desc_sw128(asa + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-          mma_ts_w(tSD + 64 * sb + 32, tV + kk * 8, smem_desc_sw128(ada + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+            mma_ts(tSD + 64 * sb, tK + kk * 8, desc_adv(da, off), idesc_s, kk > 0 ? 1u : 0u);
+            mma_ts(tSD + 64 * sb + 32, tV + kk * 8, desc_adv(dd, off), idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.sfull[sb]);
         }
-        mma_commit_w(&sm.sfull[sb]);
+        __syncwarp();
       };
       issue_s(0);
       if (nquart > 1) issue_s(1);
@@ -1320,14 +1324,18 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int t = Q >> 2, q = Q & 3, buf = t & 1, sb = Q & 1;
         mbar_wait(&sm.pready[sb], (Q >> 1) & 1);
         tc_fence_after();
-        const uint32_t asa = smem_u32(sm.as[buf]), ada = smem_u32(sm.adp[buf]);
+        const uint64_t da = smem_desc_sw128(smem_u32(sm.as[buf]), kPanelBytes, 1024);
+        const uint64_t dd = smem_desc_sw128(smem_u32(sm.adp[buf]), kPanelBytes, 1024);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {  // dV += P^T A_dP, dK += dS^T A_S over the quarter's 32 rows
-          const uint32_t acc = (Q > 0 || kk > 0) ? 1u : 0u;
-          const uint32_t roff = (32 * q + 16 * kk) * 128;
-          mma_ts_w(tdV, tSD + 64 * sb + 8 * kk, smem_desc_sw128(ada + roff, kPanelBytes, 1024), idesc_acc, acc);
-          mma_ts_w(tdK, tSD + 64 * sb + 32 + 8 * kk, smem_desc_sw128(asa + roff, kPanelBytes, 1024), idesc_acc, acc);
+          for (int kk = 0; kk < 2; ++kk) {  // dV += P^T A_dP, dK += dS^T A_S over the quarter's 32 rows
+            const uint32_t acc = (Q > 0 || kk > 0) ? 1u : 0u;
+            const uint32_t roff = (32 * q + 16 * kk) * 128;
+            mma_ts(tdV, tSD + 64 * sb + 8 * kk, desc_adv(dd, roff), idesc_acc, acc);
+            mma_ts(tdK, tSD + 64 * sb + 32 + 8 * kk, desc_adv(da, roff), idesc_acc, acc);
+          }
         }
+        __syncwarp();
         if (q == 3) {
           mma_commit_w(&sm.afree[buf]);
           SA_TRACE_AT(lane == 0 && t >= 50 && t < 53, 4, trn, t << 16 | 41 << 8);

@@ -180,14 +180,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_s = [&](int c, int x) {
         const int s = (kc + c) % kStages;
         const uint32_t idesc_s = idesc_f16(128, chunk_width(it, c), 0, 0);
-        const uint32_t kaddr = smem_u32(sm.k[s]);
+        const uint64_t dk = smem_desc_sw128(smem_u32(sm.k[s]), 16, 1024);
+        if (elect_one()) {  // one thread issues the group (descriptors advance in uniform registers)
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
-          mma_ts_w(tbase + kColS0 + 64 * x, tbase + kColA0 + 64 * x + kk * 8, smem_desc_sw128(kaddr + off, 16, 1024),
-                   idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+            mma_ts(tbase + kColS0 + 64 * x, tbase + kColA0 + 64 * x + kk * 8, desc_adv(dk, off), idesc_s,
+                   kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.sfull[x]);
         }
-        mma_commit_w(&sm.sfull[x]);
+        __syncwarp();
       };
       mbar_wait(&sm.aready[0], gc & 1);
       mbar_wait(&sm.aready[1], gc & 1);
@@ -205,9 +208,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&sm.pready[x], (kc + c) & 1);
           tc_fence_after();
           SA_TRACE_AT(trm, 0, trn, tn << 16 | (11 + x) << 8 | c);
-          for (int kk = 0; kk < w / 16; ++kk)
-            mma_ts_w(tbase + kColU0 + 128 * x, tbase + kColS0 + 64 * x + kk * 8,
-                     smem_desc_sw128(vaddr + kk * 16 * 128, kPanelBytes, 1024), idesc_pv, (c > 0 || kk > 0) ? 1u : 0u);
+          const uint64_t dv = smem_desc_sw128(vaddr, kPanelBytes, 1024);
+          if (elect_one()) {
+            for (int kk = 0; kk < w / 16; ++kk)
+              mma_ts(tbase + kColU0 + 128 * x, tbase + kColS0 + 64 * x + kk * 8, desc_adv(dv, kk * 16 * 128), idesc_pv,
+                     (c > 0 || kk > 0) ? 1u : 0u);
+          }
+          __syncwarp();
           if (c + 1 < it.nch) {
             if (x == 0) {
               mbar_wait(&sm.kvfull[(kc + c + 1) % kStages], ((kc + c + 1) / kStages) & 1);
