@@ -90,12 +90,12 @@ struct QSmem {
   alignas(1024) uint8_t v[kStages][kStageBytes];
   float acc_k2[RING][D];
   float acc_v2[RING][D];
-  union {
+  alignas(16) union {
     struct {
       float eq[128][25], ek[128][25], ev[128][25];
     } g;  // generic passes (PW <= 24)
     struct {
-      float ek[128][33], ev[128][33];
+      float ek[128][36], ev[128][36];  // 16-byte aligned rows (float4 traffic, conflict-free)
     } w;  // R = 32 trilinear passes (PW = 32, dq reduced in registers)
   } eb;
   // staged rows; pitch D+8 halves so that lanes reading consecutive rows hit distinct banks
@@ -333,14 +333,18 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
     for (int e = 0; e < 8; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
   }
   tmem_ld_wait();
-  float v[8];
+  float v[8], ck[8], cv[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const float w = __uint_as_float(uw[e]);
     v[e] = s * k2v[e] * w;
-    sm.eb.w.ek[r][8 * m + e] = s * qv[e] * w;
-    sm.eb.w.ev[r][8 * m + e] = dov[e] * __uint_as_float(uu[e]);
+    ck[e] = s * qv[e] * w;
+    cv[e] = dov[e] * __uint_as_float(uu[e]);
   }
+  *reinterpret_cast<float4*>(&sm.eb.w.ek[r][8 * m]) = make_float4(ck[0], ck[1], ck[2], ck[3]);
+  *reinterpret_cast<float4*>(&sm.eb.w.ek[r][8 * m + 4]) = make_float4(ck[4], ck[5], ck[6], ck[7]);
+  *reinterpret_cast<float4*>(&sm.eb.w.ev[r][8 * m]) = make_float4(cv[0], cv[1], cv[2], cv[3]);
+  *reinterpret_cast<float4*>(&sm.eb.w.ev[r][8 * m + 4]) = make_float4(cv[4], cv[5], cv[6], cv[7]);
   // reduce-scatter the 8 columns over the 32 lanes: after the xor-16/8/4 stages lane L holds column
   // (L>>4)&1 | ((L>>3)&1)<<1 | ((L>>2)&1)<<2 summed over 8 lanes; xor 2 and 1 finish the sum
 #pragma unroll
@@ -369,23 +373,38 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
 #ifdef SA_ABLATE_GATHER
   if (nsl > 0) return;
 #endif
-  for (int idx = tidc; idx < nsl * 32; idx += kQNT) {
-    const int sl = idx >> 5, d = idx & 31;
+  // key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g); thread -> (sl, 4 columns)
+  for (int idx = tidc; idx < nsl * 8; idx += kQNT) {
+    const int sl = idx >> 3, d = 4 * (idx & 7);
     const int kp = P0 - a.R + 1 + sl;
     const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
-    float tk[4], tv[4];
+    float4 tk[4], tv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {  // G = 4 for R = 32
       const int gg = glo + u;
       const int row = (gg << 5) + (sl - gg);
-      tk[u] = gg <= ghi ? sm.eb.w.ek[row][d] : 0.f;
-      tv[u] = gg <= ghi ? sm.eb.w.ev[row][d] : 0.f;
+      tk[u] = tv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gg <= ghi) {
+        tk[u] = *reinterpret_cast<const float4*>(&sm.eb.w.ek[row][d]);
+        tv[u] = *reinterpret_cast<const float4*>(&sm.eb.w.ev[row][d]);
+      }
     }
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
     if (kp >= 0) {
-      sm.acc_k2[slot][c0 + d] += (tk[0] + tk[1]) + (tk[2] + tk[3]);
-      sm.acc_v2[slot][c0 + d] += (tv[0] + tv[1]) + (tv[2] + tv[3]);
+      float4* ak = reinterpret_cast<float4*>(&sm.acc_k2[slot][c0 + d]);
+      float4* av = reinterpret_cast<float4*>(&sm.acc_v2[slot][c0 + d]);
+      float4 xk = *ak, xv = *av;
+      xk.x += (tk[0].x + tk[1].x) + (tk[2].x + tk[3].x);
+      xk.y += (tk[0].y + tk[1].y) + (tk[2].y + tk[3].y);
+      xk.z += (tk[0].z + tk[1].z) + (tk[2].z + tk[3].z);
+      xk.w += (tk[0].w + tk[1].w) + (tk[2].w + tk[3].w);
+      xv.x += (tv[0].x + tv[1].x) + (tv[2].x + tv[3].x);
+      xv.y += (tv[0].y + tv[1].y) + (tv[2].y + tv[3].y);
+      xv.z += (tv[0].z + tv[1].z) + (tv[2].z + tv[3].z);
+      xv.w += (tv[0].w + tv[1].w) + (tv[2].w + tv[3].w);
+      *ak = xk;
+      *av = xv;
     }
   }
   named_bar_sync(1, kQNT);
