@@ -215,6 +215,60 @@ def run_reference(args, c):
     print(json.dumps(line), flush=True)
 
 
+# Table 1 of the paper: latency of the (w1, w2) pairs it reports, on its (unstated) shape.
+TABLE1 = [(1024, 32, 104.1), (512, 64, 110.7), (128, 128, 59.2), (256, 64, 55.8), (512, 32, 55.1),
+          (1024, 16, 55.1), (256, 32, 28.3)]
+
+
+def run_table1(args, c):
+    """Re-measure the paper's only kernel experiment on B200: fwd+bwd latency and TFLOP/s (paper
+    basis) of each (w1, w2) pair at config c's B, H, N, D; the paper's ms are quoted as context
+    (their shape and hardware are not stated, so they are not a like-for-like baseline)."""
+    import paper_2507_02754_b200 as sa
+    dev = torch.device("cuda", 0)
+    B, H, N, D, det = (c[k] for k in ("B", "H", "N", "D", "det"))
+    inp = make_inputs(B, N, H, D, seed_of(args.config), dtype=c["dtype"], device="cpu")
+    t = {n: x.to(dev) for n, x in inp.items()}
+    stream = torch.cuda.current_stream(dev)
+    for w1, w2, paper_ms in TABLE1:
+        cc = dict(c, w1=w1, w2=w2)
+
+        def fwd():
+            return sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2, det=det)
+
+        def bwd(o, lse):
+            sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2, det=det)
+
+        steps = max(1, args.steps)
+        for _ in range(max(1, args.warmup)):
+            o, lse = fwd()
+            bwd(o, lse)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        fms = bms = 0.0
+        for _ in range(steps):
+            e[0].record(stream)
+            o, lse = fwd()
+            e[1].record(stream)
+            bwd(o, lse)
+            e[2].record(stream)
+            torch.cuda.synchronize()
+            fms += e[0].elapsed_time(e[1])
+            bms += e[1].elapsed_time(e[2])
+        fms, bms = fms / steps, bms / steps
+        fl = paper_flops(cc)
+        print(json.dumps({
+            "sweep": "table1", "w1": w1, "w2": w2, "w1xw2": w1 * w2,
+            "config": f"B={B} H={H} N={N} D={D} {'det' if det else 'trilinear'} bf16",
+            "fwd_ms": fms, "bwd_ms": bms, "ms_per_step": fms + bms,
+            "tflops_paper_basis": fl / ((fms + bms) / 1e3) / 1e12,
+            "fwd_tflops": paper_flops(cc, ("fwd",)) / (fms / 1e3) / 1e12,
+            "paths": {"fwd": {1: "simt", 2: "tcgen05"}.get(sa.fwd_path(B, H, N, D, w1, w2, det=det)),
+                      "bwd": {1: "simt", 2: "tcgen05"}.get(sa.bwd_path(B, H, N, D, w1, w2, det=det))},
+            "paper_latency_ms": paper_ms, "paper_note": "paper's shape/hardware unstated (P:335-354); context only",
+        }), flush=True)
+
+
 def config_block(c, n, mode="bh"):
     return {"workload": f"{c['name']}: B={c['B']} H={c['H']} N={c['N']} D={c['D']} w1={c['w1']} w2={c['w2']} "
                         f"{'det' if c['det'] else 'trilinear'} {'fwd+bwd' if c['bwd'] else 'fwd'} per GPU",
@@ -237,6 +291,9 @@ def main():
     ap.add_argument("--out-f32", action="store_true", help="write o/grads in fp32 (parity runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", default=None, choices=["table1"],
+                    help="table1: the paper's (w1, w2) latency sweep (Table 1, P:335-354) at the chosen "
+                         "config's B, H, N, D; one JSON line per pair (not the bench line)")
     ap.add_argument("--mode", default="bh", choices=["bh", "seq"],
                     help="bh: each rank runs its own B*H shard (weak scaling, no collective); seq: the "
                          "sequence is split across ranks (N per rank fixed) with the NCCL halo exchange")
@@ -245,6 +302,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, c)
+        return
+    if args.sweep == "table1":
+        run_table1(args, c)
         return
 
     import paper_2507_02754_b200 as sa
