@@ -47,7 +47,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescale = 8.0f;  // log2 units: rescale U only when the row max grows by > 2^8
 constexpr uint32_t kColS0 = 0, kColU0 = 128, kColA0 = 384;
-constexpr int kStgRows = 96;  // staged rows per pair (2G + 2(R+2G-1) <= 96: R in {16, 32})
+constexpr int kStgRows = 140;  // staged rows per pair (2G + 2(R+2G-1) <= 140: R in {16, 32, 64})
 
 struct FwdArgs {
   Problem p;                // after the (K,V,w1) <-> (K',V',w2) swap: w2 = rows per query
@@ -480,6 +480,80 @@ __global__ void __launch_bounds__(kThreads, 1)
               reinterpret_cast<float*>(a.o)[off] = v[0] * invL;
             else
               reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(v[0] * invL);
+          }
+        }
+      } else if (a.R == 64) {
+        // one query == two warps (lane quarters qd, qd^1): warp-level statistics by shuffles, the
+        // partner's partials through shared memory; each warp reduce-scatters its 32 rows, the even
+        // warp adds the odd warp's column partials and writes o
+        const bool live = valid && m_ref != -INFINITY;
+        float M = live ? m_ref : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        if (lane == 0) sm.gM[x][qd] = M;
+        named_bar_sync(1 + x, 128);
+        M = fmaxf(M, sm.gM[x][qd ^ 1]);
+        const float crow = live ? ex2(m_ref - M) : 0.f;
+        float L = live ? l * crow : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        if (lane == 0) sm.gL[x][qd] = L;
+        named_bar_sync(1 + x, 128);
+        L += sm.gL[x][qd ^ 1];
+        const bool qlive = g < nq;
+        const bool lead = (qd & 1) == 0;
+        if (lead && lane == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
+        const float invL = qlive ? 1.f / L : 0.f;
+#pragma unroll 1
+        for (int cb = 0; cb < D / 16; ++cb) {
+          uint32_t u[16];
+          tmem_ld16(tU + 16 * cb, u);
+          tmem_ld_wait();
+          float v[16];
+          if (valid) {
+            if (STAGED) {
+              const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
+#pragma unroll
+              for (int t = 0; t < 2; ++t) {
+                const uint4 y = vp[t];
+                const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = bf16x2_to_f2(ys[e]);
+                  v[8 * t + 2 * e] = f.x;
+                  v[8 * t + 2 * e + 1] = f.y;
+                }
+              }
+            } else {
+              load_bf16<16>(v2row + 16 * cb, v);
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] *= crow * __uint_as_float(u[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0.f;
+          }
+#pragma unroll
+          for (int st = 16, n = 8; st >= 2; st >>= 1, n >>= 1) {
+            const bool hi = lane & st;
+#pragma unroll
+            for (int i = 0; i < n; ++i) {
+              const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+            }
+          }
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+          const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+          float* part = &sm.ebuf[x][(cb & 1) * 4 + qd][0];  // column partials, double-buffered by cb parity
+          if (!lead && (lane & 1) == 0) part[col] = v[0];
+          named_bar_sync(1 + x, 128);
+          if (lead && (lane & 1) == 0 && qlive) {
+            const float y = v[0] + sm.ebuf[x][(cb & 1) * 4 + (qd ^ 1)][col];
+            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + col;
+            if (a.out_f32)
+              reinterpret_cast<float*>(a.o)[off] = y * invL;
+            else
+              reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(y * invL);
           }
         }
       } else {

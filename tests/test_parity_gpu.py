@@ -77,6 +77,8 @@ def test_fp32_shapes(B, N, H, D, w1, w2, det):
     (2, 256, 1, 64, 48, 16),     # D = 64
     (1, 200, 1, 128, 40, 64),    # w2 = 64
     (1, 160, 1, 128, 16, 48),    # w2 > w1
+    (1, 300, 2, 128, 128, 64),   # R = 64 rows per query (G = 2): the c5 / Table-1 (512, 64) tiling
+    (2, 170, 1, 128, 96, 64),    # R = 64, ragged tail
 ])
 def test_bf16_shapes(B, N, H, D, w1, w2, det, force_simt):
     inp = make_inputs(B, N, H, D, seed=7 * N + D, dtype="bf16")
@@ -143,7 +145,7 @@ def test_host_step_matches_device_path(B):
             assert torch.equal(h_out[n], dev[n].cpu()), n
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
 def test_baseline_config_sampled(cfg):
     """Full BASELINE sizes in the bench's launch configuration; the oracle checks sampled
     (b, h, query-range) slices window-exactly (sa_testutil.oracle_slice)."""

@@ -13,7 +13,10 @@ binding._build.build = lambda *a, **k: os.path.join(ROOT, "paper_2507_02754_b200
 L = binding.load_library()
 L.simplicial_attn_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
-c = CONFIGS[cfg]
+c = dict(CONFIGS[cfg])
+for kv in sys.argv[2:]:  # overrides, e.g. w2=64
+    k_, v_ = kv.split("=")
+    c[k_] = int(v_)
 inp = make_inputs(c["B"], c["N"], c["H"], c["D"], 1, dtype=c["dtype"])
 t = {n: x.cuda() for n, x in inp.items()}
 for rep in range(2):
