@@ -101,6 +101,7 @@ struct QSmem {
   // staged rows; pitch D+8 halves so that lanes reading consecutive rows hit distinct banks
   alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D + 8];
   float slse[2][16], sdl[2][16];
+  float dqx[2][32];  // R = 64: the odd lane quarter's dq column partials of the current pass
   uint64_t kvfull[kStages], kvempty[kStages];
   uint64_t sfull[2], pready[2], udone, aready;
   uint32_t tmem_base;
@@ -358,14 +359,19 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
   }
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  const int gq = r >> 5;
-  if ((ln & 3) == 0 && gq < it.nq) {
-    const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+  const int gq = r >> a.lR;
+  const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+  // R = 64: a query spans two lane quarters; the odd one parks its partial column sums
+  const bool lead = a.R == 32 || ((r >> 5) & 1) == 0;
+  if (!lead && (ln & 3) == 0) sm.dqx[gq][8 * m + col] = v[0];
+  if (a.R == 64) named_bar_sync(1, kQNT);
+  if (lead && (ln & 3) == 0 && gq < it.nq) {
+    const float y = a.R == 64 ? v[0] + sm.dqx[gq][8 * m + col] : v[0];
     const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + col;
     if (a.out_f32)
-      reinterpret_cast<float*>(a.dq)[off] = v[0];
+      reinterpret_cast<float*>(a.dq)[off] = y;
     else
-      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
   }
   named_bar_sync(1, kQNT);
   const int P0 = p.np + it.i0;
@@ -380,9 +386,9 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
     const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
     float4 tk[4], tv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // G = 4 for R = 32
+    for (int u = 0; u < 4; ++u) {  // G = 4 (R = 32) or 2 (R = 64) terms
       const int gg = glo + u;
-      const int row = (gg << 5) + (sl - gg);
+      const int row = (gg << a.lR) + (sl - gg);
       tk[u] = tv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (gg <= ghi) {
         tk[u] = *reinterpret_cast<const float4*>(&sm.eb.w.ek[row][d]);
@@ -563,7 +569,27 @@ __global__ void __launch_bounds__(kQThreads, 1)
     const float sl2 = p.scale * kLog2e;
     // stage tile `item`'s rows into buffer `buf` (cp.async, one group per call)
     auto stage = [&](int item, int buf) {
-      if (!STAGED) return;
+      if (!STAGED) {  // no shared-memory staging (large R): pull the next tile's rows into L2 instead
+        const QItem it = q_item(a, item);
+        const int P0 = p.np + it.i0;
+        const int nk = a.R + a.G - 1;
+        constexpr int kLines = D * 2 / 128;  // 128-byte lines per fp16 row
+        for (int task = tid256; task < (2 * a.G + 2 * nk) * kLines; task += kQNT) {
+          const int row = task / kLines, ln128 = task % kLines;
+          const __half* src = nullptr;
+          if (row < a.G) {
+            if (row < it.nq) src = a.q + p.qoff(it.b, it.i0 + row, it.h);
+          } else if (row < 2 * a.G) {
+            if (row - a.G < it.nq) src = a.dO + p.qoff(it.b, it.i0 + row - a.G, it.h);
+          } else {
+            const int rr = row - 2 * a.G;
+            const int kp = P0 - a.R + 1 + (rr < nk ? rr : rr - nk);
+            if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.koff(it.b, kp, it.h);
+          }
+          if (src) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 64 * ln128));
+        }
+        return;
+      }
       const QItem it = q_item(a, item);
       const int P0 = p.np + it.i0;
       const int nk = a.R + a.G - 1;
@@ -610,6 +636,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
           cp_async_wait<0>();
         }
         named_bar_sync(1, kQNT);
+      } else if (item + 1 < it_end) {
+        stage(item + 1, 0);  // L2 prefetch of the next tile's rows
       }
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 8 << 8);
       const bool first_in_sub = item == it_begin || it.grp == 0;
@@ -798,7 +826,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         if constexpr (D % 24 != 0)
           q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256,
                                                         sub == 0);
-      } else if (a.R == 32) {
+      } else if (a.R == 32 || a.R == 64) {
 #pragma unroll 1
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
         for (int c0 = 0; c0 < D; c0 += 32) {
