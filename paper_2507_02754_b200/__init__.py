@@ -10,3 +10,4 @@ from .binding import (  # noqa: F401
     backward, bwd_path, forward, fwd_path, host_step, launch_count, lib, load_library,
     profile_enable, profile_read,
 )
+from .autograd import SimplicialAttnFunction, simplicial_attention  # noqa: F401,E402

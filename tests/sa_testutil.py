@@ -45,3 +45,43 @@ def oracle_slice(inp: dict, b: int, h: int, a: int, L: int, w1: int, w2: int, de
             hi = end if end == N else max(a, end - w + 1)
             res[name] = (a, hi, g[0, npf + 0:npf + (hi - a), 0])
     return res
+
+
+# ---------------------------------------------------------------------------------------------
+# Match3 (Theorem 1; construction App. A) through the determinant logits.
+# ---------------------------------------------------------------------------------------------
+def match3_problem(xs, M: int, c: float, D: int = 64):
+    """Embeddings of App. A for a sequence whose position 0 is the blank token and positions
+    1..n carry xs (values in [0, M)).  Chunk 0 (dims 0-2) and chunk 1 (dims 3-5) are the paper's
+    q, k, k'; the 7th dimension of the paper's blank pair (a dot-product score the
+    kernel does not have) becomes a third determinant chunk (dims 6-8): q = (c,0,0), and only
+    the blank token has k = (0,1,0), k' = (0,0,1), so det = c for the blank pair and 0 for any
+    pair with a regular token.  Values: 1 for regular tokens, 0 for the
+    blank, so v_j1 o v'_j2 = 1 exactly for regular pairs.  Returns float64 [1, n+1, 1, D] arrays."""
+    n = len(xs)
+    N = n + 1
+    th = np.zeros(N)
+    th[1:] = 2 * np.pi * np.asarray(xs, dtype=np.float64) / M
+    q = np.zeros((N, D))
+    k = np.zeros((N, D))
+    k2 = np.zeros((N, D))
+    v = np.ones((N, D))
+    v2 = np.ones((N, D))
+    cs, sn = np.cos(th), np.sin(th)
+    q[:, 0], q[:, 1], q[:, 3], q[:, 4], q[:, 6] = c * cs, c * sn, -c * sn, c * cs, c
+    k[1:, 0], k[1:, 1], k[1:, 3], k[1:, 4] = sn[1:], cs[1:], -sn[1:], -cs[1:]
+    k2[1:, 2], k2[1:, 5] = cs[1:], -sn[1:]
+    k[0, 7], k2[0, 8] = 1.0, 1.0  # blank token (chunk 2)
+    v[0] = 0.0
+    v2[0] = 0.0
+    return {n_: a[None, :, None, :] for n_, a in (("q", q), ("k", k), ("v", v), ("k2", k2), ("v2", v2))}
+
+
+def match3_truth(xs, M: int):
+    """Causal Match3: position i (1-based in the embedded sequence) matches iff there are
+    j1, j2 in 1..i with x_i + x_j1 + x_j2 = 0 (mod M) (the kernel's windows are causal)."""
+    out = []
+    for i in range(len(xs)):
+        hit = any((xs[i] + xs[a] + xs[b]) % M == 0 for a in range(i + 1) for b in range(i + 1))
+        out.append(hit)
+    return np.array(out)

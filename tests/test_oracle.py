@@ -324,3 +324,22 @@ def test_sampled_rows(oracle_mod):
     flat_l = lse.reshape(-1)
     np.testing.assert_array_equal(ls.reshape(-1)[rows], flat_l[rows])
     assert np.isnan(ls.reshape(-1)[1])
+
+
+@pytest.mark.parametrize("M", [3, 4, 5, 6])
+def test_match3_theorem(oracle_mod, M):
+    """Theorem 1 through the oracle's determinant logits: with the App. A embeddings
+    (sa_testutil.match3_problem) the output at position i is >= 1/2 iff x_i + x_j1 + x_j2 = 0
+    (mod M) for some causal j1, j2; the softmax splits weight between the beta matching pairs
+    (value 1) and the blank pair (value 0), o = beta / (beta + 1)."""
+    from sa_testutil import match3_problem, match3_truth
+    rng = np.random.default_rng(M)
+    D = 64
+    c = 60.0 * math.sqrt(D)  # the kernel's fixed 1/sqrt(D) scale is absorbed into c
+    for _ in range(40):
+        xs = rng.integers(0, M, size=7)
+        t = match3_problem(xs, M, c, D)
+        N = t["q"].shape[1]
+        o, _ = oracle_mod.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], N, N, det=True)
+        got = o[0, 1:, 0, 0] >= 0.5 - 1e-3
+        assert np.array_equal(got, match3_truth(xs, M)), (xs, o[0, 1:, 0, 0])

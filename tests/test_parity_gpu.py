@@ -1,11 +1,14 @@
 """GPU parity: the CUDA path (through the C ABI) against the float64 oracle, element by element,
 on the same seeded inputs.  Tolerances are the north star's: max abs 1e-4 for the fp32 path,
 2e-2 for the bf16-input path (outputs written in fp32, SA_OUT_F32; reading R20)."""
+import math
+
 import numpy as np
 import pytest
 import torch
 
 import oracle
+import paper_2507_02754_b200 as sa_pkg
 from paper_2507_02754_b200 import binding as sa
 from paper_2507_02754_b200.inputs import CONFIGS, make_inputs, seed_of
 from sa_testutil import TOL_BF16, TOL_F32, f64, maxabs, oracle_slice
@@ -193,3 +196,42 @@ def test_sequence_sharded_cuda_simulated(det):
             key_acc[n][:, sl_k] += got[n]
     for n in key_acc:
         assert maxabs(key_acc[n], full[n]) <= 1e-4, n
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_autograd_wrapper(dtype):
+    """torch.autograd through simplicial_attention reproduces the direct forward/backward calls
+    (and hence the oracle): o and all five gradients, bitwise."""
+    B, N, H, D, w1, w2 = 1, 192, 2, 64, 48, 16
+    inp = make_inputs(B, N, H, D, seed=29, dtype=dtype)
+    t = {n: x.cuda() for n, x in inp.items()}
+    leaves = {n: t[n].clone().requires_grad_(True) for n in ("q", "k", "v", "k2", "v2")}
+    o = sa_pkg.simplicial_attention(leaves["q"], leaves["k"], leaves["v"], leaves["k2"], leaves["v2"], w1, w2)
+    o.backward(t["dO"])
+    o_ref, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2)
+    grads = sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o_ref, lse, t["dO"], w1, w2)
+    assert torch.equal(o, o_ref)
+    for n, g in zip(("q", "k", "v", "k2", "v2"), grads):
+        assert torch.equal(leaves[n].grad, g), n
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_match3_det_kernel(dtype):
+    """Theorem 1's Match3 construction (App. A) evaluated by the CUDA determinant path: bf16 inputs
+    on the tcgen05 kernel (M = 4: every sin/cos is exact in bf16, so the match score is exactly c)
+    and fp32 inputs on the exact path (M = 6)."""
+    from sa_testutil import match3_problem, match3_truth
+    M = 4 if dtype == "bf16" else 6
+    D = 64
+    c = 40.0 * math.sqrt(D)
+    rng = np.random.default_rng(7)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    for _ in range(8):
+        xs = rng.integers(0, M, size=31)
+        t = {n: torch.from_numpy(a).to(tdt).cuda() for n, a in match3_problem(xs, M, c, D).items()}
+        N = t["q"].shape[1]
+        o, _ = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], N, N, det=True, out_f32=True)
+        if dtype == "bf16":
+            assert sa.fwd_path(1, 1, N, D, N, N, det=True) == sa.SA_PATH_TCGEN05
+        got = o[0, 1:, 0, 0].double().cpu().numpy() >= 0.5 - 1e-3
+        assert np.array_equal(got, match3_truth(xs, M)), xs
