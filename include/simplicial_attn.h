@@ -133,6 +133,30 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
                                     int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
                                     int64_t w2, uint32_t flags, void* stream);
 
+/* Grouped-query attention (the paper's model shares K, V, K', V' across a
+ * group of 64 query heads).  q, dO, o, dq are [B,N,H,D]; k, v, k2, v2 and dk, dv, dk2,
+ * dv2 are [B,N,H_kv,D] with H_kv dividing H: query head h reads key head h / (H / H_kv), and each
+ * key-side gradient is the sum over the query heads of its group.  H_kv == H is ordinary
+ * multi-head attention.  n_prefix = 0.  Dtypes, flags, ownership and errors as for
+ * simplicial_attn_fwd / _bwd; H_kv < 1, H_kv > H or H mod H_kv != 0 -> SA_ERR_INVALID_ARG.
+ * The forward needs simplicial_attn_fwd_gqa_workspace_bytes(...) bytes of workspace (may be 0:
+ * pass any pointer).  The backward's workspace (simplicial_attn_bwd_gqa_workspace_bytes) also holds
+ * per-query-head fp32 partials of the four key-side gradients, reduced over each group at the end
+ * (deterministic: fixed summation order). */
+size_t simplicial_attn_fwd_gqa_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                               int64_t w1, int64_t w2, uint32_t flags);
+sa_status simplicial_attn_fwd_gqa(const void* q, const void* k, const void* v, const void* k2,
+                                  const void* v2, void* o, float* lse, void* workspace,
+                                  size_t workspace_bytes, int64_t B, int64_t H, int64_t H_kv, int64_t N,
+                                  int64_t D, int64_t w1, int64_t w2, uint32_t flags, void* stream);
+size_t simplicial_attn_bwd_gqa_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                               int64_t w1, int64_t w2, uint32_t flags);
+sa_status simplicial_attn_bwd_gqa(const void* q, const void* k, const void* v, const void* k2,
+                                  const void* v2, const void* o, const float* lse, const void* dO,
+                                  void* dq, void* dk, void* dv, void* dk2, void* dv2, void* workspace,
+                                  size_t workspace_bytes, int64_t B, int64_t H, int64_t H_kv, int64_t N,
+                                  int64_t D, int64_t w1, int64_t w2, uint32_t flags, void* stream);
+
 /* Which kernel family the dispatcher picks for these arguments (SA_PATH_*), 0 if unsupported. */
 int simplicial_attn_fwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
                              uint32_t flags);

@@ -14,6 +14,13 @@ forward(q, k, v, k2, v2, w1, w2, det=False, n_prefix=0) -> (o, lse)
 backward(q, k, v, k2, v2, dO, w1, w2, det=False, n_prefix=0) -> (dq, dk, dv, dk2, dv2)
     Corrected Sec. 7 equations, see DESIGN.md readings.
 
+forward_gqa(q, k, v, k2, v2, w1, w2, det=False) / backward_gqa(...)
+    Grouped-query attention (GQA ratio 64 in the paper's
+    model; head mapping S:110): key-side tensors carry H_kv heads and
+    query head h reads key head h // (H / H_kv).  Written as its definition: the
+    key heads are repeated to H and the plain oracle runs; each key-side gradient
+    is the sum of the gradients of the query heads that share it (chain rule).
+
 All arrays are float64 numpy arrays; q/dO are [B, N, H, D], key-side tensors
 are [B, n_prefix+N, H, D] (query row i sits at key position n_prefix+i).
 """
@@ -111,3 +118,23 @@ def backward(q, k, v, k2, v2, dO, w1, w2, det=False, n_prefix=0):
                           _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dk2), _ptr(dv2),
                           B, H, N, D, int(w1), int(w2), int(n_prefix), int(bool(det)))
     return dq, dk, dv, dk2, dv2
+
+
+def _repeat_heads(t: np.ndarray, r: int) -> np.ndarray:
+    return np.ascontiguousarray(np.repeat(t, r, axis=2))  # [kv0]*r, [kv1]*r, ...: head h -> h // r
+
+
+def forward_gqa(q, k, v, k2, v2, w1, w2, det=False):
+    q, k, v, k2, v2 = map(_f64, (q, k, v, k2, v2))
+    H, Hk = q.shape[2], k.shape[2]
+    assert H % Hk == 0
+    r = H // Hk
+    return forward(q, *(_repeat_heads(t, r) for t in (k, v, k2, v2)), w1, w2, det=det)
+
+
+def backward_gqa(q, k, v, k2, v2, dO, w1, w2, det=False):
+    q, k, v, k2, v2, dO = map(_f64, (q, k, v, k2, v2, dO))
+    B, NK, Hk, D = k.shape
+    r = q.shape[2] // Hk
+    dq, *gk = backward(q, *(_repeat_heads(t, r) for t in (k, v, k2, v2)), dO, w1, w2, det=det)
+    return (dq, *(g.reshape(B, NK, Hk, r, D).sum(axis=3) for g in gk))

@@ -30,6 +30,8 @@ EXPORTS = (
     "simplicial_attn_host_step", "simplicial_attn_fwd_path", "simplicial_attn_bwd_path",
     "simplicial_attn_launch_count", "simplicial_attn_status_string", "simplicial_attn_version",
     "simplicial_attn_profile_enable", "simplicial_attn_profile_read",
+    "simplicial_attn_fwd_gqa_workspace_bytes", "simplicial_attn_fwd_gqa",
+    "simplicial_attn_bwd_gqa_workspace_bytes", "simplicial_attn_bwd_gqa",
 )
 
 _lib = None
@@ -68,6 +70,10 @@ def load_library(build: bool = True):
         "simplicial_attn_profile_enable": ([ctypes.c_int], None),
         "simplicial_attn_profile_read": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_int64), ctypes.c_int], ctypes.c_int),
+        "simplicial_attn_fwd_gqa_workspace_bytes": ([I] * 7 + [U], S),
+        "simplicial_attn_fwd_gqa": ([P] * 8 + [S] + [I] * 7 + [U, P], ctypes.c_int),
+        "simplicial_attn_bwd_gqa_workspace_bytes": ([I] * 7 + [U], S),
+        "simplicial_attn_bwd_gqa": ([P] * 14 + [S] + [I] * 7 + [U, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -111,16 +117,17 @@ def _out_dtype(flags: int) -> torch.dtype:
     return torch.float32 if flags & (SA_IN_F32 | SA_OUT_F32) else torch.bfloat16
 
 
-def _check_inputs(q, keys, n_prefix):
+def _check_inputs(q, keys, n_prefix, h_kv=None):
     if not q.is_cuda:
         raise SimplicialAttnError("simplicial_attn needs CUDA tensors (there is no CPU path)")
     B, N, H, D = q.shape
+    Hk = H if h_kv is None else h_kv
     for t in (q, *keys):
         if not t.is_contiguous() or t.dtype != q.dtype or t.device != q.device:
             raise SimplicialAttnError("inputs must be contiguous, same dtype and device")
     for t in keys:
-        if tuple(t.shape) != (B, N + n_prefix, H, D):
-            raise SimplicialAttnError(f"key-side tensor shape {tuple(t.shape)} != {(B, N + n_prefix, H, D)}")
+        if tuple(t.shape) != (B, N + n_prefix, Hk, D):
+            raise SimplicialAttnError(f"key-side tensor shape {tuple(t.shape)} != {(B, N + n_prefix, Hk, D)}")
     return B, N, H, D
 
 
@@ -140,12 +147,23 @@ def _workspace(device, nbytes: int, kind: str = "fwd") -> torch.Tensor:
 
 def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool = False,
             n_prefix: int = 0, force_simt: bool = False):
-    """o, lse = 2-simplicial attention forward (simplicial_attn_fwd_prefixed)."""
-    B, N, H, D = _check_inputs(q, (k, v, k2, v2), n_prefix)
+    """o, lse = 2-simplicial attention forward (simplicial_attn_fwd_prefixed; key-side tensors with
+    fewer heads than q -> grouped-query simplicial_attn_fwd_gqa)."""
+    h_kv = k.shape[2] if k.dim() == 4 and k.shape[2] != q.shape[2] else None
+    B, N, H, D = _check_inputs(q, (k, v, k2, v2), n_prefix, h_kv)
     L = lib()
     flags = _flags(q.dtype, det, out_f32, force_simt)
     o = torch.empty((B, N, H, D), dtype=_out_dtype(flags), device=q.device)
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
+    if h_kv is not None:
+        if n_prefix:
+            raise SimplicialAttnError("grouped-query mode takes no key prefix")
+        wsb = int(L.simplicial_attn_fwd_gqa_workspace_bytes(B, H, h_kv, N, D, w1, w2, flags))
+        ws = _workspace(q.device, wsb)
+        st = L.simplicial_attn_fwd_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
+                                       _ptr(ws), ws.numel(), B, H, h_kv, N, D, w1, w2, flags, _stream(q.device))
+        _check(st, "simplicial_attn_fwd_gqa")
+        return o, lse
     wsb = int(L.simplicial_attn_fwd_workspace_bytes(B, H, N, D, w1, w2, n_prefix, flags))
     ws = _workspace(q.device, wsb)
     st = L.simplicial_attn_fwd_ws(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
@@ -156,8 +174,10 @@ def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool 
 
 def backward(q, k, v, k2, v2, o, lse, dO, w1: int, w2: int, det: bool = False, out_f32: bool = False,
              n_prefix: int = 0, force_simt: bool = False, workspace: torch.Tensor | None = None):
-    """dq, dk, dv, dk2, dv2 = 2-simplicial attention backward (simplicial_attn_bwd_prefixed)."""
-    B, N, H, D = _check_inputs(q, (k, v, k2, v2), n_prefix)
+    """dq, dk, dv, dk2, dv2 = 2-simplicial attention backward (simplicial_attn_bwd_prefixed; key-side
+    tensors with fewer heads than q -> grouped-query simplicial_attn_bwd_gqa)."""
+    h_kv = k.shape[2] if k.dim() == 4 and k.shape[2] != q.shape[2] else None
+    B, N, H, D = _check_inputs(q, (k, v, k2, v2), n_prefix, h_kv)
     L = lib()
     flags = _flags(q.dtype, det, out_f32, force_simt)
     od = _out_dtype(flags)
@@ -165,6 +185,16 @@ def backward(q, k, v, k2, v2, o, lse, dO, w1: int, w2: int, det: bool = False, o
         raise SimplicialAttnError("o must be in the output dtype and dO in the input dtype, contiguous")
     dq = torch.empty((B, N, H, D), dtype=od, device=q.device)
     dk, dv, dk2, dv2 = (torch.empty_like(k, dtype=od) for _ in range(4))
+    if h_kv is not None:
+        if n_prefix:
+            raise SimplicialAttnError("grouped-query mode takes no key prefix")
+        wsb = int(L.simplicial_attn_bwd_gqa_workspace_bytes(B, H, h_kv, N, D, w1, w2, flags))
+        ws = _workspace(q.device, wsb, "bwd_gqa")
+        st = L.simplicial_attn_bwd_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
+                                       _ptr(dO), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dk2), _ptr(dv2),
+                                       _ptr(ws), ws.numel(), B, H, h_kv, N, D, w1, w2, flags, _stream(q.device))
+        _check(st, "simplicial_attn_bwd_gqa")
+        return dq, dk, dv, dk2, dv2
     wsb = int(L.simplicial_attn_bwd_workspace_bytes_prefixed(B, H, N, D, w1, w2, n_prefix, flags))
     if workspace is None or workspace.numel() < wsb:
         workspace = _workspace(q.device, wsb, "bwd")

@@ -98,10 +98,30 @@ static sa_status make_problem(int64_t B, int64_t H, int64_t N, int64_t D, int64_
   if (w2 > NK) w2 = NK;
   p->B = int(B); p->H = int(H); p->N = int(N); p->D = int(D);
   p->w1 = int(w1); p->w2 = int(w2); p->np = int(n_prefix);
+  p->Hk = int(H);
+  p->hk_shift = 0;
   p->det = (flags & SA_VARIANT_DET) != 0;
   p->scale = float(1.0 / sqrt(double(D)));
   return SA_OK;
 }
+
+// Grouped-query problem: H query heads, Hk key/value heads, Hk | H (query head h reads key head
+// h / (H / Hk)).
+static sa_status make_problem_gqa(int64_t B, int64_t H, int64_t Hk, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                  uint32_t flags, Problem* p) {
+  sa_status s = make_problem(B, H, N, D, w1, w2, 0, flags, p);
+  if (s != SA_OK) return s;
+  if (Hk < 1 || Hk > H || H % Hk != 0) return SA_ERR_INVALID_ARG;
+  p->Hk = int(Hk);
+  const int64_t r = H / Hk;
+  p->hk_shift = (r & (r - 1)) == 0 ? __builtin_ctzll(uint64_t(r)) : -1;
+  return SA_OK;
+}
+
+cudaError_t gqa_reduce(const float* part, void* out, bool out_f32, int64_t rows, int Hk, int r, int D,
+                       cudaStream_t st);
+cudaError_t cast_f32_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
+cudaError_t cast_bf16_f32(const void* a, float* b, int64_t n, cudaStream_t st);
 
 static bool use_tc_fwd(const Problem& p, uint32_t flags) {
   if (flags & (SA_IN_F32 | SA_FORCE_SIMT)) return false;
@@ -413,5 +433,116 @@ int simplicial_attn_debug_trace(unsigned long long* host, int max_pairs) {
   return n;
 }
 #endif
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------------
+// Grouped-query attention
+// ------------------------------------------------------------------------------------------------
+namespace sa {
+// bwd_gqa workspace: [o fp32 (bf16 outputs only)] [dq fp32 (bf16 outputs only)]
+//                    [dk, dv, dk2, dv2 per-query-head fp32 partials] [the backward's own workspace]
+static size_t gqa_bwd_layout(const Problem& p, uint32_t flags, size_t off[8]) {
+  const bool out_f32 = (flags & (SA_IN_F32 | SA_OUT_F32)) != 0;
+  const size_t nq = size_t(p.B) * p.N * p.H * p.D, nkp = size_t(p.B) * p.NK() * p.H * p.D;
+  size_t cur = 0;
+  off[0] = cur;
+  cur += out_f32 ? 0 : align256(nq * 4);
+  off[1] = cur;
+  cur += out_f32 ? 0 : align256(nq * 4);
+  for (int t = 0; t < 4; ++t) {
+    off[2 + t] = cur;
+    cur += align256(nkp * 4);
+  }
+  off[6] = cur;
+  cur += bwd_ws(p, flags | SA_OUT_F32);
+  off[7] = cur;
+  return cur;
+}
+}  // namespace sa
+
+extern "C" {
+
+size_t simplicial_attn_fwd_gqa_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                               int64_t w1, int64_t w2, uint32_t flags) {
+  Problem p;
+  if (make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p) != SA_OK) return 0;
+  return use_tc_fwd(p, flags) ? tc_fwd_workspace_bytes(p) : 0;
+}
+
+sa_status simplicial_attn_fwd_gqa(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                                  void* o, float* lse, void* workspace, size_t workspace_bytes, int64_t B,
+                                  int64_t H, int64_t H_kv, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                  uint32_t flags, void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse) return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p);
+  if (s != SA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  cudaGetLastError();
+  if (use_tc_fwd(p, flags)) {
+    if (!workspace || workspace_bytes < tc_fwd_workspace_bytes(p)) return SA_ERR_WORKSPACE;
+    return cuda_status(tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, workspace, st));
+  }
+  return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
+}
+
+size_t simplicial_attn_bwd_gqa_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                               int64_t w1, int64_t w2, uint32_t flags) {
+  Problem p;
+  if (make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p) != SA_OK) return 0;
+  if (p.Hk == p.H) return bwd_ws(p, flags);
+  size_t off[8];
+  return gqa_bwd_layout(p, flags, off);
+}
+
+sa_status simplicial_attn_bwd_gqa(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                                  const void* o, const float* lse, const void* dO, void* dq, void* dk, void* dv,
+                                  void* dk2, void* dv2, void* workspace, size_t workspace_bytes, int64_t B,
+                                  int64_t H, int64_t H_kv, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                  uint32_t flags, void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse || !dO || !dq || !dk || !dv || !dk2 || !dv2 || !workspace)
+    return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p);
+  if (s != SA_OK) return s;
+  if (p.Hk == p.H)
+    return simplicial_attn_bwd(q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2, workspace, workspace_bytes, B, H,
+                               N, D, w1, w2, flags, stream);
+  size_t off[8];
+  if (workspace_bytes < gqa_bwd_layout(p, flags, off)) return SA_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
+  const uint32_t flags32 = flags | SA_OUT_F32;
+  char* w = (char*)workspace;
+  const int64_t nq = int64_t(p.B) * p.N * p.H * p.D;
+  cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  // the kernels run with fp32 outputs: o as fp32, dq and the per-query-head key partials in fp32
+  const void* o32 = o;
+  float* dq32 = (float*)dq;
+  if (!out_f32) {
+    e = cast_bf16_f32(o, (float*)(w + off[0]), nq, st);
+    o32 = w + off[0];
+    dq32 = (float*)(w + off[1]);
+  }
+  float* part[4];
+  for (int t = 0; t < 4; ++t) part[t] = (float*)(w + off[2 + t]);
+  void* bw = w + off[6];
+  const size_t bwb = off[7] - off[6];
+  if (e == cudaSuccess) {
+    if (use_tc_bwd(p, flags32))
+      e = tc_backward(p, true, q, k, v, k2, v2, o32, lse, dO, dq32, part[0], part[1], part[2], part[3], bw, bwb, st);
+    else
+      e = simt_backward(p, in_f32, true, q, k, v, k2, v2, o32, lse, dO, dq32, part[0], part[1], part[2], part[3],
+                        (float*)bw, st);
+  }
+  void* outs[4] = {dk, dv, dk2, dv2};
+  for (int t = 0; t < 4 && e == cudaSuccess; ++t)
+    e = gqa_reduce(part[t], outs[t], out_f32, int64_t(p.B) * p.NK(), p.Hk, p.H / p.Hk, p.D, st);
+  if (e == cudaSuccess && !out_f32) e = cast_f32_bf16(dq32, dq, nq, st);
+  return cuda_status(e);
+}
 
 }  // extern "C"

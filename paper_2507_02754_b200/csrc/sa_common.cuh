@@ -12,16 +12,29 @@ namespace sa {
 // Problem description handed to every kernel.  Key-side tensors have NK = np + N rows.
 struct Problem {
   int B, H, N, D, w1, w2, np;  // np = n_prefix
+  int Hk;                      // key/value heads (GQA: query head h reads key head h / (H / Hk)); = H otherwise
+  int hk_shift;                // log2(H / Hk) when that ratio is a power of two (the usual case), else -1
   float scale;                 // signed logit scale (negated when the DET operands are swapped)
   bool det;
   __host__ __device__ int NK() const { return np + N; }
-  // element offsets of row (b, pos, h) in query-side / key-side tensors
+  __host__ __device__ int hk(int h) const { return hk_shift >= 0 ? h >> hk_shift : h / (H / Hk); }
+  // element offsets of row (b, pos, h) in query-side tensors and in per-query-head key-side
+  // tensors (gradient partials: [B, NK, H, D]) ...
   __host__ __device__ int64_t qoff(int b, int i, int h) const {
     return ((int64_t(b) * N + i) * H + h) * D;
   }
   __host__ __device__ int64_t koff(int b, int j, int h) const {
     return ((int64_t(b) * NK() + j) * H + h) * D;
   }
+  // ... and of the key row that query head h reads in the key-side inputs ([B, NK, Hk, D])
+  __host__ __device__ int64_t kroff(int b, int j, int h) const {
+    return ((int64_t(b) * NK() + j) * Hk + hk(h)) * D;
+  }
+  // the same with the key head already resolved (hot loops: resolve once per work item)
+  __host__ __device__ int64_t kvoff(int b, int j, int hkv) const {
+    return ((int64_t(b) * NK() + j) * Hk + hkv) * D;
+  }
+  __host__ __device__ size_t nkey() const { return size_t(B) * NK() * Hk * D; }
 };
 
 __device__ __forceinline__ float ld_f(const float* p) { return __ldg(p); }

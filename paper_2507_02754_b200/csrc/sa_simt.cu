@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads) simt_fwd(Problem p, const TIn* __res
   for (int t = 0; t < NV; ++t) O[t] = 0.f;
 
   for (int kk = k0 + warp; kk <= pos; kk += kWarps) {
-    load_row_smem(k2 + p.koff(b, kk, h), p.D, lane, sk2[warp]);
+    load_row_smem(k2 + p.kroff(b, kk, h), p.D, lane, sk2[warp]);
     __syncwarp();
     float a[NV];
     row_operand<NV>(p, sq, sk2[warp], lane, a);
@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(kThreads) simt_fwd(Problem p, const TIn* __res
     for (int t = 0; t < NV; ++t) U[t] = 0.f;
     for (int j = j0; j <= pos; ++j) {
       float kr[NV], vr[NV];
-      load_row<TIn, NV>(k + p.koff(b, j, h), p.D, lane, kr);
-      load_row<TIn, NV>(v + p.koff(b, j, h), p.D, lane, vr);
+      load_row<TIn, NV>(k + p.kroff(b, j, h), p.D, lane, kr);
+      load_row<TIn, NV>(v + p.kroff(b, j, h), p.D, lane, vr);
       float x = warp_sum(dot_lane<NV>(a, kr));
       float mn = fmaxf(m, x);
       float alpha = expf(m - mn), pj = expf(x - mn);
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kThreads) simt_fwd(Problem p, const TIn* __res
       m = mn;
     }
     float v2r[NV];
-    load_row<TIn, NV>(v2 + p.koff(b, kk, h), p.D, lane, v2r);
+    load_row<TIn, NV>(v2 + p.kroff(b, kk, h), p.D, lane, v2r);
     float Mn = fmaxf(M, m), ca = expf(M - Mn), cb = expf(m - Mn);
 #pragma unroll
     for (int t = 0; t < NV; ++t) O[t] = O[t] * ca + cb * v2r[t] * U[t];
@@ -199,11 +199,11 @@ __global__ void __launch_bounds__(kThreads) simt_bwd_dq(Problem p, const TIn* __
 #pragma unroll
   for (int t = 0; t < NV; ++t) acc[t] = 0.f;
   for (int kk = k0 + warp; kk <= pos; kk += kWarps) {
-    load_row_smem(k2 + p.koff(b, kk, h), p.D, lane, sk2[warp]);
+    load_row_smem(k2 + p.kroff(b, kk, h), p.D, lane, sk2[warp]);
     __syncwarp();
     float a[NV], g[NV], W[NV];
     row_operand<NV>(p, sq, sk2[warp], lane, a);
-    load_row<TIn, NV>(v2 + p.koff(b, kk, h), p.D, lane, g);
+    load_row<TIn, NV>(v2 + p.kroff(b, kk, h), p.D, lane, g);
 #pragma unroll
     for (int t = 0; t < NV; ++t) {
       int d = lane + 32 * t;
@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(kThreads) simt_bwd_dq(Problem p, const TIn* __
     }
     for (int j = j0; j <= pos; ++j) {
       float kr[NV], vr[NV];
-      load_row<TIn, NV>(k + p.koff(b, j, h), p.D, lane, kr);
-      load_row<TIn, NV>(v + p.koff(b, j, h), p.D, lane, vr);
+      load_row<TIn, NV>(k + p.kroff(b, j, h), p.D, lane, kr);
+      load_row<TIn, NV>(v + p.kroff(b, j, h), p.D, lane, vr);
       float x = warp_sum(dot_lane<NV>(a, kr));
       float y = warp_sum(dot_lane<NV>(g, vr));
       float ds = expf(x - li) * (y - Di);
@@ -256,10 +256,10 @@ __global__ void __launch_bounds__(kThreads) simt_bwd_dk2(Problem p, const TIn* _
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ float sk2[32 * NV];
   __shared__ float sqw[kWarps][32 * NV], sW[kWarps][32 * NV];
-  for (int d = threadIdx.x; d < p.D; d += kThreads) sk2[d] = ld_f(k2 + p.koff(b, kk, h) + d);
+  for (int d = threadIdx.x; d < p.D; d += kThreads) sk2[d] = ld_f(k2 + p.kroff(b, kk, h) + d);
   __syncthreads();
   float v2r[NV];
-  load_row<TIn, NV>(v2 + p.koff(b, kk, h), p.D, lane, v2r);
+  load_row<TIn, NV>(v2 + p.kroff(b, kk, h), p.D, lane, v2r);
   const int D3 = (p.D / 3) * 3;
   float ak[NV], av[NV];
 #pragma unroll
@@ -278,8 +278,8 @@ __global__ void __launch_bounds__(kThreads) simt_bwd_dk2(Problem p, const TIn* _
     for (int t = 0; t < NV; ++t) { g[t] = dor[t] * v2r[t]; W[t] = U[t] = 0.f; }
     for (int j = win_lo(pos, p.w1); j <= pos; ++j) {
       float kr[NV], vr[NV];
-      load_row<TIn, NV>(k + p.koff(b, j, h), p.D, lane, kr);
-      load_row<TIn, NV>(v + p.koff(b, j, h), p.D, lane, vr);
+      load_row<TIn, NV>(k + p.kroff(b, j, h), p.D, lane, kr);
+      load_row<TIn, NV>(v + p.kroff(b, j, h), p.D, lane, vr);
       float x = warp_sum(dot_lane<NV>(a, kr));
       float y = warp_sum(dot_lane<NV>(g, vr));
       float pj = expf(x - li);
@@ -328,8 +328,8 @@ __global__ void __launch_bounds__(kThreads) simt_bwd_dk(Problem p, const TIn* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ float sqw[kWarps][32 * NV], sk2w[kWarps][32 * NV];
   float kr[NV], vr[NV];
-  load_row<TIn, NV>(k + p.koff(b, j, h), p.D, lane, kr);
-  load_row<TIn, NV>(v + p.koff(b, j, h), p.D, lane, vr);
+  load_row<TIn, NV>(k + p.kroff(b, j, h), p.D, lane, kr);
+  load_row<TIn, NV>(v + p.kroff(b, j, h), p.D, lane, vr);
   float ak[NV], av[NV];
 #pragma unroll
   for (int t = 0; t < NV; ++t) ak[t] = av[t] = 0.f;
@@ -343,11 +343,11 @@ __global__ void __launch_bounds__(kThreads) simt_bwd_dk(Problem p, const TIn* __
     load_row<TIn, NV>(dO + p.qoff(b, i, h), p.D, lane, dor);
     for (int kk = win_lo(pos, p.w2); kk <= pos; ++kk) {
       __syncwarp();
-      load_row_smem(k2 + p.koff(b, kk, h), p.D, lane, sk2w[warp]);
+      load_row_smem(k2 + p.kroff(b, kk, h), p.D, lane, sk2w[warp]);
       __syncwarp();
       float a[NV], g[NV];
       row_operand<NV>(p, sqw[warp], sk2w[warp], lane, a);
-      load_row<TIn, NV>(v2 + p.koff(b, kk, h), p.D, lane, g);
+      load_row<TIn, NV>(v2 + p.kroff(b, kk, h), p.D, lane, g);
 #pragma unroll
       for (int t = 0; t < NV; ++t) g[t] *= dor[t];
       float x = warp_sum(dot_lane<NV>(a, kr));

@@ -108,7 +108,7 @@ struct QSmem {
 };
 
 struct QItem {
-  int bh, b, h, grp, i0, nq, jbeg, span, nch;
+  int bh, b, h, hk, grp, i0, nq, jbeg, span, nch;  // hk: the key head query head h reads (GQA)
 };
 
 __device__ __forceinline__ QItem q_item(const BwdQArgs& a, int item) {
@@ -117,6 +117,7 @@ __device__ __forceinline__ QItem q_item(const BwdQArgs& a, int item) {
   it.grp = item % a.ngroups;
   it.b = it.bh / a.p.H;
   it.h = it.bh % a.p.H;
+  it.hk = a.p.hk(it.h);
   it.i0 = it.grp * a.G;
   it.nq = min(a.G, a.p.N - it.i0);
   const int pos0 = a.p.np + it.i0, posl = pos0 + it.nq - 1;
@@ -469,8 +470,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
           mbar_wait(&sm.kvempty[s], ph ^ 1);
           mbar_expect_tx(&sm.kvfull[s], 2 * Sm::kStageBytes);
           for (int pn = 0; pn < kPanels; ++pn) {
-            tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.h, row, it.b);
-            tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.h, row, it.b);
+            tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.hk, row, it.b);
+            tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.hk, row, it.b);
           }
         }
       }
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           } else {
             const int rr = row - 2 * a.G;
             const int kp = P0 - a.R + 1 + (rr < nk ? rr : rr - nk);
-            if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.koff(it.b, kp, it.h);
+            if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.kvoff(it.b, kp, it.hk);
           }
           if (src) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 64 * ln128));
         }
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         } else {
           const int rr = row - 2 * a.G;
           const int kp = P0 - a.R + 1 + (rr < nk ? rr : rr - nk);
-          if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.koff(it.b, kp, it.h);
+          if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.kvoff(it.b, kp, it.hk);
         }
         if (src) cp_async16(&sm.stg[buf][row][8 * c8], src + 8 * c8);
       }
@@ -674,8 +675,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
         } else {
           rw.q = a.q + p.qoff(it.b, it.i0 + g, it.h);
           rw.dO = a.dO + p.qoff(it.b, it.i0 + g, it.h);
-          rw.k2 = a.k2 + p.koff(it.b, kpos, it.h);
-          rw.v2 = a.v2 + p.koff(it.b, kpos, it.h);
+          rw.k2 = a.k2 + p.kvoff(it.b, kpos, it.hk);
+          rw.v2 = a.v2 + p.kvoff(it.b, kpos, it.hk);
         }
       }
       // ---- row operands (fp16, unscaled): half 0 -> A_S = q o k2 [det: k2 x q], half 1 -> A_dP = dO o v2 ----
@@ -992,7 +993,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
   constexpr int kPanels = D / 64;
   constexpr uint32_t kPanelBytes = KVSmem<D>::kPanelBytes;
   constexpr int kC8 = D / 8;  // 16-byte chunks per row
-  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
+  const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H, hkv = p.hk(h);
   const int j0 = blockIdx.x * 128;
   // queries touching key rows [j0, j0+128): positions [j0, j0+127+w1-1] within [np, np+N)
   const int qa = max(j0, p.np) - p.np;
@@ -1037,7 +1038,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           if (kp < 0 || kp >= p.NK()) continue;
           int slot = slo + off;
           if (slot >= a.ring) slot -= a.ring;
-          const __half* src = (which ? a.v2 : a.k2) + p.koff(b, kp, h) + 8 * c8;
+          const __half* src = (which ? a.v2 : a.k2) + p.kvoff(b, kp, hkv) + 8 * c8;
           __half* dst = (which ? &sm.rv2[0][0] : &sm.rk2[0][0]) + slot * D + 8 * c8;
           cp_async16(dst, src);
         }
@@ -1213,8 +1214,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             int slot = sbase + g + kk;
             if (slot >= a.ring) slot -= a.ring;
             if (ok[u]) {
-              const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
-              const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
+              const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.kvoff(b, kpos, hkv);
+              const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.kvoff(b, kpos, hkv);
               yk[u] = *reinterpret_cast<const uint4*>(k2row + 8 * c8);
               wv[u] = *reinterpret_cast<const uint4*>(v2row + 8 * c8);
             }
@@ -1253,8 +1254,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         if (slot >= a.ring) slot -= a.ring;
         const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
         const __half* dorow = STAGED ? &sm.sdo[buf][g][0] : a.dO + p.qoff(b, i, h);
-        const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.koff(b, kpos, h);
-        const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.koff(b, kpos, h);
+        const __half* k2row = STAGED ? &sm.rk2[slot][0] : a.k2 + p.kvoff(b, kpos, hkv);
+        const __half* v2row = STAGED ? &sm.rv2[slot][0] : a.v2 + p.kvoff(b, kpos, hkv);
         if (!DET) {
           uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
           if (valid) {
@@ -1417,7 +1418,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 #pragma unroll
       for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
       if (j < p.NK()) {
-        const uint4* src = reinterpret_cast<const uint4*>((wg == 0 ? a.k : a.v) + p.koff(b, j, h));
+        const uint4* src = reinterpret_cast<const uint4*>((wg == 0 ? a.k : a.v) + p.kvoff(b, j, hkv));
 #pragma unroll
         for (int t = 0; t < D / 8; ++t) {
           const uint4 x = src[t];
@@ -1593,7 +1594,7 @@ size_t tc_bwd_workspace_bytes(const Problem& p0) {
   const int R = p.w2, G = 128 / R;
   int pc, items;
   const int grid = q_grid(p, R, G, &pc, &items);
-  const size_t n = size_t(p.B) * p.NK() * p.H * p.D, nq = size_t(p.B) * p.N * p.H * p.D;
+  const size_t n = p.nkey(), nq = size_t(p.B) * p.N * p.H * p.D;
   return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 4 * a256(n * 2) + 2 * a256(nq * 2) +
          a256(sizeof(float) * size_t(grid) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
 }
@@ -1612,7 +1613,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   }
   if (ws_bytes < tc_bwd_workspace_bytes(p0)) return cudaErrorInvalidValue;
   const int R = p.w2, G = 128 / R;
-  const size_t n = size_t(p.B) * p.NK() * p.H * p.D;
+  const size_t n = p.nkey();
   char* w = (char*)ws;
   float* delta = (float*)w;
   w += a256(sizeof(float) * size_t(p.B) * p.H * p.N);
@@ -1649,8 +1650,8 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   // bwd_q: dq, dk2, dv2
   {
     CUtensorMap tmK, tmV;
-    if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.H, p.D, kQChunk) ||
-        !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.H, p.D, kQChunk))
+    if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.Hk, p.D, kQChunk) ||
+        !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.Hk, p.D, kQChunk))
       return cudaErrorInvalidValue;
     BwdQArgs a;
     a.p = p;

@@ -96,7 +96,7 @@ struct Smem {
 };
 
 struct Item {
-  int b, h, pair, jbeg, span, nch;
+  int b, h, hk, pair, jbeg, span, nch;  // hk: the key head query head h reads (GQA)
 };
 
 __device__ __forceinline__ Item get_item(const FwdArgs& a, int item) {
@@ -105,6 +105,7 @@ __device__ __forceinline__ Item get_item(const FwdArgs& a, int item) {
   it.pair = item % a.npairs;
   it.b = bh / a.p.H;
   it.h = bh % a.p.H;
+  it.hk = a.p.hk(it.h);
   const int i0 = 2 * it.pair * a.G;
   const int iend = min(a.p.N, i0 + 2 * a.G);  // exclusive
   const int pos0 = a.p.np + i0, posl = a.p.np + iend - 1;
@@ -162,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&sm.kvempty[s], ph ^ 1);
           mbar_expect_tx(&sm.kvfull[s], 2 * Smem<D>::kStageBytes);
           for (int pn = 0; pn < kPanels; ++pn) {
-            tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.h, row, it.b);
-            tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.h, row, it.b);
+            tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.hk, row, it.b);
+            tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.hk, row, it.b);
           }
         }
       }
@@ -259,8 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int rr = row - 2 * a.G;
           const int kp = kb + (rr < nk2 ? rr : rr - nk2);
           if (kp >= 0 && kp < p.NK())
-            src = rr < nk2 ? (const void*)(a.k2 + p.koff(it.b, kp, it.h) + 8 * c8)
-                           : (const void*)(a.v2 + p.koff(it.b, kp, it.h) + 8 * c8);
+            src = rr < nk2 ? (const void*)(a.k2 + p.kvoff(it.b, kp, it.hk) + 8 * c8)
+                           : (const void*)(a.v2 + p.kvoff(it.b, kp, it.hk) + 8 * c8);
         }
         if (src) cp_async16(&sm.stg[buf][row][8 * c8], src);
       }
@@ -295,8 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __half* qrow = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][x * a.G + g][0])
                                   : a.q + p.qoff(it.b, i0 + g, it.h);
       const __half* k2row = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][2 * a.G + srow][0])
-                                   : a.k2 + p.koff(it.b, kpos, it.h);
-      const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2 + srow][0] : a.v2 + p.koff(it.b, kpos, it.h);
+                                   : a.k2 + p.kvoff(it.b, kpos, it.hk);
+      const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2 + srow][0] : a.v2 + p.kvoff(it.b, kpos, it.hk);
 
       // ---- A operand a_(i,k) = s log2e (q_i o k2_k)  [det: s log2e (k2_k x q_i)], fp16 -> TMEM ----
       {
@@ -643,7 +644,7 @@ bool tc_fwd_supported(const Problem& p) {
 }
 
 size_t tc_fwd_workspace_bytes(const Problem& p) {
-  const size_t n = size_t(p.B) * p.NK() * p.H * p.D, nq = size_t(p.B) * p.N * p.H * p.D;
+  const size_t n = p.nkey(), nq = size_t(p.B) * p.N * p.H * p.D;
   return 3 * ((n * 2 + 255) & ~size_t(255)) + ((nq * 2 + 255) & ~size_t(255));
 }
 
@@ -656,7 +657,7 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
     std::swap(p.w1, p.w2);
     if (p.det) p.scale = -p.scale;
   }
-  const size_t n = size_t(p.B) * p.NK() * p.H * p.D;
+  const size_t n = p.nkey();
   const size_t nq = size_t(p.B) * p.N * p.H * p.D;
   char* kf = (char*)ws;
   char* vf = kf + ((n * 2 + 255) & ~size_t(255));
@@ -666,8 +667,8 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
   if (e == cudaSuccess) e = convert_two_f16(q, qf, int64_t(nq), k2, k2f, int64_t(n), num_sms(), st);
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmV;
-  if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.H, p.D, kChunk) ||
-      !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.H, p.D, kChunk))
+  if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.Hk, p.D, kChunk) ||
+      !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.Hk, p.D, kChunk))
     return cudaErrorInvalidValue;
   FwdArgs a;
   a.p = p;

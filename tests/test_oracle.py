@@ -343,3 +343,25 @@ def test_match3_theorem(oracle_mod, M):
         o, _ = oracle_mod.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], N, N, det=True)
         got = o[0, 1:, 0, 0] >= 0.5 - 1e-3
         assert np.array_equal(got, match3_truth(xs, M)), (xs, o[0, 1:, 0, 0])
+
+
+@pytest.mark.parametrize("H,Hk,det", [(4, 2, False), (4, 1, True), (6, 3, False)])
+def test_gqa_against_autograd(oracle_mod, H, Hk, det):
+    """Grouped-query oracle (forward_gqa / backward_gqa) against torch autograd of the dense
+    Alg. 1 model whose key heads are expanded with repeat_interleave: autograd forms the
+    group sums of the key-side gradients itself (S:110 head mapping h -> h // (H / H_kv))."""
+    B, N, D, w1, w2 = 2, 10, 6, 5, 3
+    rng = np.random.default_rng(H * 10 + Hk)
+    q = rng.standard_normal((B, N, H, D))
+    dO = rng.standard_normal((B, N, H, D))
+    keys = [rng.standard_normal((B, N, Hk, D)) for _ in range(4)]
+    o, _ = oracle_mod.forward_gqa(q, *keys, w1, w2, det=det)
+    grads = oracle_mod.backward_gqa(q, *keys, dO, w1, w2, det=det)
+    tq = torch.tensor(q, requires_grad=True)
+    tk = [torch.tensor(x, requires_grad=True) for x in keys]
+    exp = [t.repeat_interleave(H // Hk, dim=2) for t in tk]
+    ro = dense_torch(tq, *exp, w1, w2, det=det)
+    ro.backward(torch.tensor(dO))
+    assert np.max(np.abs(o - ro.detach().numpy())) < 1e-12
+    for g, t in zip(grads, [tq, *tk]):
+        assert np.max(np.abs(g - t.grad.numpy())) < 1e-10

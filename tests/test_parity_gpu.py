@@ -235,3 +235,33 @@ def test_match3_det_kernel(dtype):
             assert sa.fwd_path(1, 1, N, D, N, N, det=True) == sa.SA_PATH_TCGEN05
         got = o[0, 1:, 0, 0].double().cpu().numpy() >= 0.5 - 1e-3
         assert np.array_equal(got, match3_truth(xs, M)), xs
+
+
+@pytest.mark.parametrize("dtype,tol", [("bf16", TOL_BF16), ("f32", TOL_F32)])
+@pytest.mark.parametrize("H,Hk,D,w1,w2,det", [
+    (4, 2, 128, 96, 32, False),   # tcgen05 path, ratio 2
+    (8, 1, 64, 64, 16, True),     # all query heads share one key head (det)
+    (4, 4, 128, 64, 32, False),   # H_kv == H: the ordinary path through the GQA entry points
+])
+def test_gqa(dtype, tol, H, Hk, D, w1, w2, det):
+    """Grouped-query entry points against the grouped-query oracle (expand + group sums)."""
+    B, N = 2, 200
+    g = torch.Generator().manual_seed(H * 100 + Hk)
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q, dO = (torch.randn(B, N, H, D, generator=g).to(dt) for _ in range(2))
+    keys = [torch.randn(B, N, Hk, D, generator=g).to(dt) for _ in range(4)]
+    t = [x.to(DEV) for x in (q, *keys, dO)]
+    o, lse = sa.forward(*t[:5], w1, w2, det=det, out_f32=True)
+    grads = sa.backward(*t[:5], o, lse, t[5], w1, w2, det=det, out_f32=True)
+    torch.cuda.synchronize()
+    a = [f64(x) for x in (q, *keys, dO)]
+    ro, rl = oracle.forward_gqa(*a[:5], w1, w2, det=det)
+    rg = oracle.backward_gqa(*a[:5], a[5], w1, w2, det=det)
+    got = dict(zip(("o", "lse", "dq", "dk", "dv", "dk2", "dv2"), (o, lse, *grads)))
+    ref = dict(zip(("o", "lse", "dq", "dk", "dv", "dk2", "dv2"), (ro, rl, *rg)))
+    assert_close(got, ref, tol)
+    if Hk < H:  # bf16 outputs: the reduction writes the output dtype
+        o16, lse16 = sa.forward(*t[:5], w1, w2, det=det)
+        g16 = sa.backward(*t[:5], o16, lse16, t[5], w1, w2, det=det)
+        assert all(x.dtype == (torch.bfloat16 if dtype == "bf16" else torch.float32) for x in g16)
+        assert maxabs(g16[1], rg[1]) <= 4 * TOL_BF16
