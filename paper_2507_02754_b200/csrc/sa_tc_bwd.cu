@@ -622,24 +622,132 @@ __global__ void __launch_bounds__(kQThreads, 1)
     uint32_t kc = 0, gc = 0;
     int PS = 0, flush_lo = 0;
     int trn = 0;
-    if (it_begin < it_end) stage(it_begin, 0);
+    // ---- row operands of tile `fitem` (fp16, unscaled): half 0 -> A_S = q o k2 [det: k2 x q],
+    //      half 1 -> A_dP = dO o v2, from staging buffer `bf`.  Formed for tile t+1 right after the
+    //      chunk loop of tile t (the A regions are free then), so the S/dP MMAs of t+1 overlap the
+    //      epilogue of t. ----
+    auto form_A = [&](int fitem, int bf) {
+      const QItem fi = q_item(a, fitem);
+      const int fP0 = p.np + fi.i0;
+      const int g = r >> a.lR, kk = r & (a.R - 1);
+      const int fkpos = fP0 + g - a.R + 1 + kk;
+      const bool fvalid = r < a.G * a.R && g < fi.nq && fkpos >= 0;
+      QRows fr{};
+      if (fvalid) {
+        const int nk = a.R + a.G - 1;
+        if (STAGED) {
+          fr.q = &sm.stg[bf][g][0];
+          fr.dO = &sm.stg[bf][a.G + g][0];
+          fr.k2 = &sm.stg[bf][2 * a.G + g + kk][0];
+          fr.v2 = &sm.stg[bf][2 * a.G + nk + g + kk][0];
+        } else {
+          fr.q = a.q + p.qoff(fi.b, fi.i0 + g, fi.h);
+          fr.dO = a.dO + p.qoff(fi.b, fi.i0 + g, fi.h);
+          fr.k2 = a.k2 + p.kvoff(fi.b, fkpos, fi.hk);
+          fr.v2 = a.v2 + p.kvoff(fi.b, fkpos, fi.hk);
+        }
+      }
+      const bool tr = (threadIdx.x & 127) == 0 && threadIdx.x < 256 && fitem - it_begin >= 100 && fitem - it_begin < 102;
+      const int treg = 1 + half;
+        if (DET && half == 0) {
+          uint32_t pk[D / 2];
+  #pragma unroll
+          for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
+          if (fvalid && sub == 0) {
+            const __half* x = fr.q;
+            const __half* y = fr.k2;
+            {
+              constexpr int D3 = (D / 3) * 3;
+  #pragma unroll
+              for (int base = 0; base < D; base += 24) {
+                float xf[24], yf[24];
+  #pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                  if (base + 8 * u < D) {
+                    float tx[8], ty[8];
+                    load_f16<8>(x + base + 8 * u, tx);
+                    load_f16<8>(y + base + 8 * u, ty);
+  #pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                      xf[8 * u + e] = tx[e];
+                      yf[8 * u + e] = ty[e];
+                    }
+                  } else {
+  #pragma unroll
+                    for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
+                  }
+                }
+  #pragma unroll
+                for (int c3 = 0; c3 < 24; c3 += 3) {
+                  float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+                  if (base + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
+                    a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+                    a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+                    a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+                  }
+                  xf[c3] = a0;
+                  xf[c3 + 1] = a1;
+                  xf[c3 + 2] = a2;
+                }
+  #pragma unroll
+                for (int e = 0; e < 24; e += 2)
+                  if (base + e < D) pk[(base + e) / 2] = pack_f16x2(xf[e], xf[e + 1]);
+              }
+            }
+          }
+          if (sub == 0) tmem_store_row<D>(tAS, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.aready);
+        } else {
+          // trilinear (A_S = q o k2) or A_dP = dO o v2: sub-warp `sub` forms columns [D/2 sub, D/2 sub + D/2)
+          constexpr int DH = D / 2;
+          uint32_t pk[DH / 2];
+  #pragma unroll
+          for (int t = 0; t < DH / 2; ++t) pk[t] = 0u;
+          if (fvalid) {
+            const __half* x = (half == 0 ? fr.q : fr.dO) + DH * sub;
+            const __half* y = (half == 0 ? fr.k2 : fr.v2) + DH * sub;
+  #pragma unroll
+            for (int t = 0; t < DH / 8; ++t) {
+              const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * t);
+              const uint4 yv = *reinterpret_cast<const uint4*>(y + 8 * t);
+              pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
+              pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
+              pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
+              pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
+            }
+          }
+          SA_TRACE_AT(tr, treg, trn, (fitem - it_begin) << 16 | 9 << 8);
+          const uint32_t ta = (half == 0 ? tAS : tAdP) + (DH / 2) * sub;
+          if constexpr (DH == 64)
+            tmem_st32(ta, pk);
+          else
+            tmem_st16(ta, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.aready);
+          SA_TRACE_AT(tr, treg, trn, (fitem - it_begin) << 16 | 2 << 8);
+        }
+    };
+    if (it_begin < it_end) {
+      stage(it_begin, 0);
+      if (STAGED) {
+        cp_async_wait<0>();
+        named_bar_sync(1, kQNT);
+      }
+      form_A(it_begin, 0);
+    }
     for (int item = it_begin; item < it_end; ++item) {
       QItem it = q_item(a, item);
       const bool tr = (threadIdx.x & 127) == 0 && threadIdx.x < 256 && item - it_begin >= 100 && item - it_begin < 102;
       const int treg = 1 + half;
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 1 << 8);
       const int buf = STAGED ? int(gc & 1) : 0;
-      if (STAGED) {
-        if (item + 1 < it_end) {
-          stage(item + 1, buf ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        named_bar_sync(1, kQNT);
-      } else if (item + 1 < it_end) {
-        stage(item + 1, 0);  // L2 prefetch of the next tile's rows
-      }
+      // this tile's rows were staged (and waited for) before its A operands were formed; prefetch the next
+      if (item + 1 < it_end) stage(item + 1, STAGED ? (buf ^ 1) : 0);
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 8 << 8);
       const bool first_in_sub = item == it_begin || it.grp == 0;
       const bool last_in_sub = item == it_end - 1 || it.grp == a.ngroups - 1;
@@ -678,89 +786,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
           rw.k2 = a.k2 + p.kvoff(it.b, kpos, it.hk);
           rw.v2 = a.v2 + p.kvoff(it.b, kpos, it.hk);
         }
-      }
-      // ---- row operands (fp16, unscaled): half 0 -> A_S = q o k2 [det: k2 x q], half 1 -> A_dP = dO o v2 ----
-      if (DET && half == 0) {
-        uint32_t pk[D / 2];
-#pragma unroll
-        for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
-        if (valid && sub == 0) {
-          const __half* x = rw.q;
-          const __half* y = rw.k2;
-          {
-            constexpr int D3 = (D / 3) * 3;
-#pragma unroll
-            for (int base = 0; base < D; base += 24) {
-              float xf[24], yf[24];
-#pragma unroll
-              for (int u = 0; u < 3; ++u) {
-                if (base + 8 * u < D) {
-                  float tx[8], ty[8];
-                  load_f16<8>(x + base + 8 * u, tx);
-                  load_f16<8>(y + base + 8 * u, ty);
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) {
-                    xf[8 * u + e] = tx[e];
-                    yf[8 * u + e] = ty[e];
-                  }
-                } else {
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
-                }
-              }
-#pragma unroll
-              for (int c3 = 0; c3 < 24; c3 += 3) {
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-                if (base + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
-                  a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
-                  a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
-                  a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
-                }
-                xf[c3] = a0;
-                xf[c3 + 1] = a1;
-                xf[c3 + 2] = a2;
-              }
-#pragma unroll
-              for (int e = 0; e < 24; e += 2)
-                if (base + e < D) pk[(base + e) / 2] = pack_f16x2(xf[e], xf[e + 1]);
-            }
-          }
-        }
-        if (sub == 0) tmem_store_row<D>(tAS, pk);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.aready);
-      } else {
-        // trilinear (A_S = q o k2) or A_dP = dO o v2: sub-warp `sub` forms columns [D/2 sub, D/2 sub + D/2)
-        constexpr int DH = D / 2;
-        uint32_t pk[DH / 2];
-#pragma unroll
-        for (int t = 0; t < DH / 2; ++t) pk[t] = 0u;
-        if (valid) {
-          const __half* x = (half == 0 ? rw.q : rw.dO) + DH * sub;
-          const __half* y = (half == 0 ? rw.k2 : rw.v2) + DH * sub;
-#pragma unroll
-          for (int t = 0; t < DH / 8; ++t) {
-            const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * t);
-            const uint4 yv = *reinterpret_cast<const uint4*>(y + 8 * t);
-            pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
-            pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
-            pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
-            pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
-          }
-        }
-        SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 9 << 8);
-        const uint32_t ta = (half == 0 ? tAS : tAdP) + (DH / 2) * sub;
-        if constexpr (DH == 64)
-          tmem_st32(ta, pk);
-        else
-          tmem_st16(ta, pk);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.aready);
-        SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 2 << 8);
       }
       // ---- chunks: P = exp(S - lse), dS = P (dP - delta), this half's 32 columns ----
       const int jlo = max(0, pos - p.w1 + 1);
@@ -815,6 +840,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pready[half]);
         SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 4 << 8 | c);
+      }
+      // ---- A operands of the next tile (its S/dP MMAs then run during this tile's epilogue) ----
+      if (item + 1 < it_end) {
+        if (STAGED) cp_async_wait<0>();
+        named_bar_sync(1, kQNT);  // every warp is past its last S/dP wait: the A regions are free
+        form_A(item + 1, STAGED ? (buf ^ 1) : 0);
       }
       // ---- epilogue ----
       mbar_wait(&sm.udone, gc & 1);
