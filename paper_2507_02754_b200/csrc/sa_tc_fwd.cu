@@ -269,22 +269,69 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     uint32_t cc = 0, gc = 0;
     int trn = 0;
-    if (blockIdx.x < a.items) stage(blockIdx.x, 0);
+    // ---- A operand of pair `fitem` from staging buffer `bf`: a_(i,k) = q_i o k2_k (trilinear,
+    //      unscaled) [det: s log2e (k2_k x q_i)], fp16 -> TMEM.  Formed for pair n+1 right after the
+    //      chunk loop of pair n (the A regions are free then), so the first S MMAs of n+1 overlap the
+    //      epilogue of n. ----
+    auto form_A = [&](int fitem, int bf) {
+      const Item fit = get_item(a, fitem);
+      const int fi0 = (2 * fit.pair + x) * a.G;
+      const int fnq = max(0, min(a.G, p.N - fi0));
+      const int fkpos = p.np + fi0 + g - a.R + 1 + kk;
+      const bool fvalid = r < a.G * a.R && g < fnq && fkpos >= 0;
+      const __half* fq = STAGED ? reinterpret_cast<const __half*>(&sm.stg[bf][x * a.G + g][0])
+                                : a.q + p.qoff(fit.b, fi0 + g, fit.h);
+      const __half* fk2 = STAGED ? reinterpret_cast<const __half*>(&sm.stg[bf][2 * a.G + x * a.G + g + kk][0])
+                                 : a.k2 + p.kvoff(fit.b, fkpos, fit.hk);
+      const int ftn = fitem / gridDim.x;
+      const bool ftrs = r == 0 && ftn >= 50 && ftn < 52;
+        {
+          uint32_t pk[D / 2];
+  #pragma unroll
+          for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
+          if (fvalid) {
+            if (p.det) {
+              row_operand_from_f16<D>(fq, fk2, a.a_scale, pk);
+            } else {  // unscaled q o k2 (the scale is applied by the softmax FFMA)
+              const uint4* xp = reinterpret_cast<const uint4*>(fq);
+              const uint4* yp = reinterpret_cast<const uint4*>(fk2);
+  #pragma unroll
+              for (int t = 0; t < D / 8; ++t) {
+                const uint4 xv = xp[t], yv = yp[t];
+                pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
+                pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
+                pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
+                pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
+              }
+            }
+          }
+          SA_TRACE_AT(ftrs, 1 + x, trn, ftn << 16 | 29 << 8);
+          tmem_store_row<D>(tA, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.aready[x]);
+          SA_TRACE_AT(ftrs, 1 + x, trn, ftn << 16 | 21 << 8);
+        }
+
+    };
+    if (blockIdx.x < a.items) {
+      stage(blockIdx.x, 0);
+      if (STAGED) {
+        cp_async_wait<0>();
+        named_bar_sync(3, 256);
+      }
+      form_A(blockIdx.x, 0);
+    }
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
       const Item it = get_item(a, item);
       const int tn = item / gridDim.x;
       const bool trs = r == 0 && tn >= 50 && tn < 52;
       SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 20 << 8);
       const int buf = STAGED ? int(gc & 1) : 0;
-      if (STAGED) {
-        if (item + int(gridDim.x) < a.items) {
-          stage(item + gridDim.x, buf ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        named_bar_sync(3, 256);
-      }
+      const int nitem = item + int(gridDim.x);
+      // this pair's rows were staged (and waited for) before its A operands were formed; prefetch the next
+      if (nitem < a.items) stage(nitem, buf ^ 1);
       SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 28 << 8);
       const int i0 = (2 * it.pair + x) * a.G;
       const int nq = max(0, min(a.G, p.N - i0));
@@ -298,36 +345,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __half* k2row = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][2 * a.G + srow][0])
                                    : a.k2 + p.kvoff(it.b, kpos, it.hk);
       const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2 + srow][0] : a.v2 + p.kvoff(it.b, kpos, it.hk);
-
-      // ---- A operand a_(i,k) = s log2e (q_i o k2_k)  [det: s log2e (k2_k x q_i)], fp16 -> TMEM ----
-      {
-        uint32_t pk[D / 2];
-#pragma unroll
-        for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
-        if (valid) {
-          if (p.det) {
-            row_operand_from_f16<D>(qrow, k2row, a.a_scale, pk);
-          } else {  // unscaled q o k2 (the scale is applied by the softmax FFMA)
-            const uint4* xp = reinterpret_cast<const uint4*>(qrow);
-            const uint4* yp = reinterpret_cast<const uint4*>(k2row);
-#pragma unroll
-            for (int t = 0; t < D / 8; ++t) {
-              const uint4 xv = xp[t], yv = yp[t];
-              pk[4 * t + 0] = hmul2_u32(xv.x, yv.x);
-              pk[4 * t + 1] = hmul2_u32(xv.y, yv.y);
-              pk[4 * t + 2] = hmul2_u32(xv.z, yv.z);
-              pk[4 * t + 3] = hmul2_u32(xv.w, yv.w);
-            }
-          }
-        }
-        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 29 << 8);
-        tmem_store_row<D>(tA, pk);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.aready[x]);
-        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 21 << 8);
-      }
 
       // ---- chunks: per-row online softmax (conditional rescaling) ----
       float m_ref = -INFINITY, l = 0.f;
@@ -417,6 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 25 << 8 | c);
       }
 
+      // ---- A operand of the next pair (its first S MMAs then run during this pair's epilogue) ----
+      if (nitem < a.items) {
+        if (STAGED) cp_async_wait<0>();
+        named_bar_sync(3, 256);  // every softmax warp is past its last S wait: the A regions are free
+        form_A(nitem, buf ^ 1);
+      }
       // ---- epilogue: merge the R rows of each query, v2 o U, normalise ----
       mbar_wait(&sm.udone[x], gc & 1);
       tc_fence_after();
