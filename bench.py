@@ -83,7 +83,7 @@ def kernel_traffic(name: str, c: dict):
     newest committed `ncu --set full` summary for this config (profiles/*_traffic_<cfg>.json,
     written by tools/profile_summarize.py), or (None, reason)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_traffic_{c['name']}.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_traffic_{c['name']}.json")))  # newest tag sorts last
     for fn in reversed(files):
         k = json.load(open(fn)).get("kernels", {}).get(name)
         if k:
