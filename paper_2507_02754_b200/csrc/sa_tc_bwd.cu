@@ -527,7 +527,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
           const uint32_t kaddr = smem_u32(sm.k[s]), vaddr = smem_u32(sm.v[s]);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            mbar_wait(&sm.pready[hh], (kc + c) & 1);
+            // P/dS of this half ready: the 8 softmax warps of the half bar.arrive on named barrier
+            // 2+hh; the MMA warp blocks in bar.sync (no polling)
+            named_bar_sync(2 + hh, 32 * 8 + 32);
             tc_fence_after();
             SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | (11 + hh) << 8 | c);
             const int nwh = min(32, w - 32 * hh);
@@ -838,7 +840,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pready[half]);
+        named_bar_arrive(2 + half, 32 * 8 + 32);
         SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 4 << 8 | c);
       }
       // ---- A operands of the next tile (its S/dP MMAs then run during this tile's epilogue) ----
