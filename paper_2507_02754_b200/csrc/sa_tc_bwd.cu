@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       for (int item = it_begin; item < it_end; ++item) {
         QItem it = q_item(a, item);
         const bool trm = lane == 0 && item - it_begin >= 100 && item - it_begin < 102;
-        mbar_wait(&sm.aready, gc & 1);
+        named_bar_sync(4, kQNT + 32);  // A operands formed (all compute warps bar.arrive)
         SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | 10 << 8);
         tc_fence_after();
         // Issue order per chunk c and half hh (hh = column halves [32hh, 32hh+32) of a 64-row chunk):
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.aready);
+          named_bar_arrive(4, kQNT + 32);
         } else {
           // trilinear (A_S = q o k2) or A_dP = dO o v2: sub-warp `sub` forms columns [D/2 sub, D/2 sub + D/2)
           constexpr int DH = D / 2;
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.aready);
+          named_bar_arrive(4, kQNT + 32);
           SA_TRACE_AT(tr, treg, trn, (fitem - it_begin) << 16 | 2 << 8);
         }
     };
@@ -1403,7 +1403,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       bool early = false;
       for (int Q = 0; Q < nquart; ++Q) {
         const int t = Q >> 2, q = Q & 3, buf = t & 1, sb = Q & 1;
-        mbar_wait(&sm.pready[sb], (Q >> 1) & 1);
+        named_bar_sync(3 + sb, 4 * 32 + 32);  // P/dS of quarter Q ready (warpgroup sb bar.arrives)
         tc_fence_after();
         const uint64_t da = smem_desc_sw128(smem_u32(sm.as[buf]), kPanelBytes, 1024);
         const uint64_t dd = smem_desc_sw128(smem_u32(sm.adp[buf]), kPanelBytes, 1024);
@@ -1529,7 +1529,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.pready[wg]);
+      named_bar_arrive(3 + wg, 4 * 32 + 32);
       SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (54 + q) << 8);
     }
     const int half = wg;

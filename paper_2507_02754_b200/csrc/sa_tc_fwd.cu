@@ -193,8 +193,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
-      mbar_wait(&sm.aready[0], gc & 1);
-      mbar_wait(&sm.aready[1], gc & 1);
+      // A operands of both tiles formed: the 8 softmax warps bar.arrive on named barriers 6/7, the MMA
+      // warp blocks in bar.sync (no mbarrier polling)
+      named_bar_sync(6, 4 * 32 + 32);
+      named_bar_sync(7, 4 * 32 + 32);
       SA_TRACE_AT(trm, 0, trn, tn << 16 | 10 << 8);
       mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
       tc_fence_after();
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t vaddr = smem_u32(sm.v[s]);
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
-          mbar_wait(&sm.pready[x], (kc + c) & 1);
+          named_bar_sync(4 + x, 4 * 32 + 32);  // P of tile x ready (4 softmax warps arrive)
           tc_fence_after();
           SA_TRACE_AT(trm, 0, trn, tn << 16 | (11 + x) << 8 | c);
           const uint64_t dv = smem_desc_sw128(vaddr, kPanelBytes, 1024);
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.aready[x]);
+          named_bar_arrive(6 + x, 4 * 32 + 32);
           SA_TRACE_AT(ftrs, 1 + x, trn, ftn << 16 | 21 << 8);
         }
 
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pready[x]);
+        named_bar_arrive(4 + x, 4 * 32 + 32);
         SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 25 << 8 | c);
       }
 
