@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const float2 xx = ffma2(make_float2(sv[2 * t], sv[2 * t + 1]), vmul, vm);
-          const float2 pv = (t & 3) == 3 ? ex2_poly2(xx) : make_float2(ex2(xx.x), ex2(xx.y));
+          const float2 pv = (t & 7) == 7 ? ex2_poly2(xx) : make_float2(ex2(xx.x), ex2(xx.y));
           ls4[t & 3] = fadd2(ls4[t & 3], pv);  // 4 independent packed partial sums
           pk[t] = pack_f16x2(pv);
         }
