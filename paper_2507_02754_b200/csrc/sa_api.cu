@@ -311,38 +311,66 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
   if (scratch_bytes < need) return SA_ERR_WORKSPACE;
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   const size_t nel = size_t(p.B) * p.N * p.H * p.D;
-  const int64_t nb = B;  // pipeline chunks: batch elements (contiguous slices of every tensor)
-  const size_t sin = nel / nb * (in_f32 ? 4 : 2), sout = nel / nb * (out_f32 ? 4 : 2);
-  const size_t slse = sizeof(float) * size_t(p.H) * p.N;
+  // Pipeline chunks: (batch b, heads [h0, h0+hc)).  Every (b,h) slice is independent.  The
+  // first and last batch elements are split into two head halves so that the exposed first upload
+  // and last download are half a batch element; the others go whole (full-size kernel launches).
+  struct Chunk {
+    int64_t b, h0, hc;
+  };
+  std::vector<Chunk> chunks;
+  for (int64_t b = 0; b < B; ++b) {
+    if ((b == 0 || b == B - 1) && H % 2 == 0) {
+      chunks.push_back({b, 0, H / 2});
+      chunks.push_back({b, H / 2, H / 2});
+    } else {
+      chunks.push_back({b, 0, H});
+    }
+  }
+  const size_t ein = in_f32 ? 4 : 2, eout = out_f32 ? 4 : 2;
+  const size_t row = size_t(D);  // elements per (position, head)
   char* base = (char*)d_scratch;
   cudaStream_t st = (cudaStream_t)stream;
   cudaGetLastError();
-  HostPipe& hp = host_pipe(int(nb));
+  HostPipe& hp = host_pipe(int(chunks.size()));
   if (!hp.ok) return SA_ERR_CUDA;
   cudaError_t e = cudaEventRecord(hp.entry, st);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.h2d, hp.entry, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.entry, 0);
-  for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
-    for (int t = 0; t < 6 && e == cudaSuccess; ++t)
-      e = cudaMemcpyAsync(base + off[t] + b * sin, (const char*)hin[t] + b * sin, sin, cudaMemcpyHostToDevice,
-                          hp.h2d);
-    if (e == cudaSuccess) e = cudaEventRecord(hp.in[b], hp.h2d);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.in[b], 0);
+  // host slice (b, heads h0..h0+hc) of a [B,N,H,D] tensor <-> compact device chunk [1,N,hc,D]
+  auto copy_in = [&](char* dst, const void* src, const Chunk& c, size_t es) {
+    const char* s0 = (const char*)src + ((c.b * N * H) + c.h0) * row * es;
+    if (c.hc == H) return cudaMemcpyAsync(dst, s0, size_t(N) * H * row * es, cudaMemcpyHostToDevice, hp.h2d);
+    return cudaMemcpy2DAsync(dst, c.hc * row * es, s0, H * row * es, c.hc * row * es, size_t(N),
+                             cudaMemcpyHostToDevice, hp.h2d);
+  };
+  auto copy_out = [&](void* dst, const char* src, const Chunk& c, size_t es) {
+    char* d0 = (char*)dst + ((c.b * N * H) + c.h0) * row * es;
+    if (c.hc == H) return cudaMemcpyAsync(d0, src, size_t(N) * H * row * es, cudaMemcpyDeviceToHost, hp.d2h);
+    return cudaMemcpy2DAsync(d0, H * row * es, src, c.hc * row * es, c.hc * row * es, size_t(N),
+                             cudaMemcpyDeviceToHost, hp.d2h);
+  };
+  for (size_t ci = 0; ci < chunks.size() && e == cudaSuccess; ++ci) {
+    const Chunk& c = chunks[ci];
+    // device chunk buffers: compact [N, hc, D] at the chunk's place inside batch element b's slice
+    const size_t cofs = size_t((c.b * H + c.h0) * N) * row;  // elements
+    auto P = [&](int t) { return base + off[t] + cofs * (t < 6 ? ein : eout); };
+    for (int t = 0; t < 6 && e == cudaSuccess; ++t) e = copy_in(P(t), hin[t], c, ein);
+    if (e == cudaSuccess) e = cudaEventRecord(hp.in[ci], hp.h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.in[ci], 0);
     if (e != cudaSuccess) break;
-    auto P = [&](int t) { return base + off[t] + b * (t < 6 ? sin : sout); };
-    float* lse_b = (float*)(base + off[7]) + b * p.H * p.N;
-    s = simplicial_attn_fwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_b, 1, H, N, D, w1, w2, flags, stream);
+    float* lse_c = (float*)(base + off[7]) + (c.b * H + c.h0) * N;
+    s = simplicial_attn_fwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, 1, c.hc, N, D, w1, w2, flags, stream);
     if (s != SA_OK) return s;
-    s = simplicial_attn_bwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_b, P(5), P(8), P(9), P(10), P(11), P(12),
-                            base + off[13], off[14] - off[13], 1, H, N, D, w1, w2, flags, stream);
+    s = simplicial_attn_bwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, P(5), P(8), P(9), P(10), P(11), P(12),
+                            base + off[13], off[14] - off[13], 1, c.hc, N, D, w1, w2, flags, stream);
     if (s != SA_OK) return s;
-    e = cudaEventRecord(hp.done[b], st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.done[b], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)h_o + b * sout, P(6), sout, cudaMemcpyDeviceToHost, hp.d2h);
+    e = cudaEventRecord(hp.done[ci], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.done[ci], 0);
+    if (e == cudaSuccess) e = copy_out(h_o, P(6), c, eout);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync((char*)h_lse + b * slse, lse_b, slse, cudaMemcpyDeviceToHost, hp.d2h);
-    for (int t = 0; t < 5 && e == cudaSuccess; ++t)
-      e = cudaMemcpyAsync((char*)hout[t] + b * sout, P(8 + t), sout, cudaMemcpyDeviceToHost, hp.d2h);
+      e = cudaMemcpyAsync((char*)h_lse + size_t((c.b * H + c.h0) * N) * 4, lse_c, size_t(c.hc) * N * 4,
+                          cudaMemcpyDeviceToHost, hp.d2h);
+    for (int t = 0; t < 5 && e == cudaSuccess; ++t) e = copy_out(hout[t], P(8 + t), c, eout);
   }
   if (e == cudaSuccess) e = cudaEventRecord(hp.out, hp.d2h);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.out, 0);
