@@ -120,7 +120,7 @@ sa_status simplicial_attn_bwd_prefixed(const void* q, const void* k, const void*
  * Host layouts/dtypes as above (n_prefix = 0).  d_scratch must hold
  * simplicial_attn_host_step_scratch_bytes(...) bytes.  The step is pipelined over chunks of
  * (batch element, heads) -- every (b,h) slice is independent; the first and last batch
- * elements are split into two head halves when H is even: the copies of chunk c+1 in and c-1 out
+ * elements are split into four (H % 4 == 0) or two head groups: the copies of chunk c+1 in and c-1 out
  * run on two library-owned copy streams while chunk c computes on `stream`.  Ordering is still that of
  * `stream`: the copies start after the work already queued on it, and `stream` waits for the last
  * device->host copy, so the results are valid once the caller syncs `stream`.  Host buffers must be

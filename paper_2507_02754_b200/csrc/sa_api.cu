@@ -318,10 +318,10 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
     int64_t b, h0, hc;
   };
   std::vector<Chunk> chunks;
+  const int64_t split = H % 4 == 0 ? 4 : (H % 2 == 0 ? 2 : 1);
   for (int64_t b = 0; b < B; ++b) {
-    if ((b == 0 || b == B - 1) && H % 2 == 0) {
-      chunks.push_back({b, 0, H / 2});
-      chunks.push_back({b, H / 2, H / 2});
+    if (b == 0 || b == B - 1) {
+      for (int64_t q = 0; q < split; ++q) chunks.push_back({b, q * (H / split), H / split});
     } else {
       chunks.push_back({b, 0, H});
     }
