@@ -1139,9 +1139,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       constexpr int kTS = (D + kWS - 1) / kWS;  // A_S tasks per row (det); trilinear fuses A_S+A_dP
       constexpr int kTasks = DET ? kTS + kC8 : kC8;
       constexpr int kRB8 = 128 * kC8 / kNF;  // rows per thread in the row-block mapping (8 at D=128)
-      if (!DET && STAGED && a.R >= kRB8) {
-        // trilinear, row blocks: thread -> (column chunk c8, kRB8 consecutive tile rows of ONE query).
+      if (STAGED && a.R >= kRB8) {
+        // row blocks: thread -> (column chunk c8, kRB8 consecutive tile rows of ONE query).
         // All loads first, then the products and the stores: no branches, kRB8-way ILP.
+        // Trilinear: A_S = q o k2 and A_dP = dO o v2 here; det: A_dP here, A_S below.
         const int c8 = ft % kC8, r0 = (ft / kC8) * kRB8;
         const int g = r0 >> a.lR, kk0 = r0 & (a.R - 1);
         const bool qok = r0 < a.G * a.R && q0 + g < qb;
@@ -1166,13 +1167,72 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
 #pragma unroll
         for (int u = 0; u < kRB8; ++u) {
-          const uint4 oa = make_uint4(hmul2_u32(xq.x, yk[u].x), hmul2_u32(xq.y, yk[u].y), hmul2_u32(xq.z, yk[u].z),
-                                      hmul2_u32(xq.w, yk[u].w));
           const uint4 od = make_uint4(hmul2_u32(ud.x, wv[u].x), hmul2_u32(ud.y, wv[u].y), hmul2_u32(ud.z, wv[u].z),
                                       hmul2_u32(ud.w, wv[u].w));
           const uint32_t dst = sw128_off(r0 + u, c8);
-          *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
+          if (!DET) {
+            const uint4 oa = make_uint4(hmul2_u32(xq.x, yk[u].x), hmul2_u32(xq.y, yk[u].y), hmul2_u32(xq.z, yk[u].z),
+                                        hmul2_u32(xq.w, yk[u].w));
+            *reinterpret_cast<uint4*>(sm.as[buf] + dst) = oa;
+          }
           *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
+        }
+        if (DET) {
+          // A_S = k2 x q (chunkwise cross products; trailing D mod 3 dims 0): tasks (row, 24-column
+          // block), kTS blocks per row, spread over all former threads
+          constexpr int D3 = (D / 3) * 3;
+          for (int task = ft; task < 128 * kTS; task += kNF) {
+            const int r = task / kTS, e0 = (task % kTS) * 24;
+            const int g2 = r >> a.lR, kk2 = r & (a.R - 1);
+            const bool ok = r < a.G * a.R && q0 + g2 < qb && kbase + g2 + kk2 >= 0;
+            uint32_t pk[12];
+#pragma unroll
+            for (int e = 0; e < 12; ++e) pk[e] = 0u;
+            if (ok) {
+              int sl = sbase + g2 + kk2;
+              if (sl >= a.ring) sl -= a.ring;
+              float xf[24], yf[24];
+#pragma unroll
+              for (int u = 0; u < 3; ++u) {
+                if (e0 + 8 * u < D) {
+                  const uint4 xv = *reinterpret_cast<const uint4*>(&sm.sq[buf][g2][e0 + 8 * u]);
+                  const uint4 yv = *reinterpret_cast<const uint4*>(&sm.rk2[sl][e0 + 8 * u]);
+                  const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 fx = __half22float2(*reinterpret_cast<const __half2*>(&xs[e]));
+                    const float2 fy = __half22float2(*reinterpret_cast<const __half2*>(&ys[e]));
+                    xf[8 * u + 2 * e] = fx.x;
+                    xf[8 * u + 2 * e + 1] = fx.y;
+                    yf[8 * u + 2 * e] = fy.x;
+                    yf[8 * u + 2 * e + 1] = fy.y;
+                  }
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
+                }
+              }
+#pragma unroll
+              for (int c3 = 0; c3 < 24; c3 += 3) {
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+                if (e0 + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
+                  a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
+                  a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
+                  a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+                }
+                xf[c3] = a0;
+                xf[c3 + 1] = a1;
+                xf[c3 + 2] = a2;
+              }
+#pragma unroll
+              for (int e = 0; e < 12; ++e) pk[e] = pack_f16x2(xf[2 * e], xf[2 * e + 1]);
+            }
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+              if (e0 + 8 * u < D)
+                *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r, e0 / 8 + u)) =
+                    make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          }
         }
         SA_TRACE_AT(trf, 3, trn, t << 16 | 34 << 8);
         SA_TRACE_AT(trf, 3, trn, t << 16 | 35 << 8);
