@@ -417,6 +417,128 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
   named_bar_sync(1, kQNT);
 }
 
+// Determinant pass over 24 columns [c0, c0+24) (eight 3-chunks), R in {32, 64}: warp m = 2 half + sub
+// of a lane quarter takes columns c0+6m..+6 (two chunks) of W (dq = s sum_k W x k2, dk2 rows
+// s q x W) and of U (dv2 rows dO o U); dq by a register reduce-scatter over the 32 lanes (six
+// values padded to eight), dk2/dv2 through the shared-memory gather in float2 pairs.  Dims past the
+// last whole chunk (D mod 3) contribute 0 (reading R5).
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_pass_det(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                                    int c0, int half, int sub, int r, bool valid, const QRows& rw,
+                                                    uint32_t tW, uint32_t tU, int tidc, int sbase) {
+  constexpr int D3 = (D / 3) * 3;
+  const Problem& p = a.p;
+  const float s = p.scale;
+  const int ln = r & 31;
+  const int m = 2 * half + sub;
+  const int cs = c0 + 6 * m;
+  const bool act = cs < D;  // warp-uniform
+  float v[8], ck[6], cv[6];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = 0.f;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) ck[e] = cv[e] = 0.f;
+  if (act) {
+    uint32_t uw[8], uu[8];
+    tmem_ld8(tW + cs, uw);
+    tmem_ld8(tU + cs, uu);
+    float k2v[6], qv[6], dov[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < 6; e += 2) {
+        if (cs + e < D) {
+          const float2 a2 = __half22float2(*reinterpret_cast<const __half2*>(rw.k2 + cs + e));
+          const float2 b2 = __half22float2(*reinterpret_cast<const __half2*>(rw.q + cs + e));
+          const float2 c2 = __half22float2(*reinterpret_cast<const __half2*>(rw.dO + cs + e));
+          k2v[e] = a2.x, k2v[e + 1] = a2.y, qv[e] = b2.x, qv[e + 1] = b2.y, dov[e] = c2.x, dov[e + 1] = c2.y;
+        }
+      }
+    }
+    tmem_ld_wait();
+    float w[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) w[e] = __uint_as_float(uw[e]);
+#pragma unroll
+    for (int t = 0; t < 6; t += 3) {
+      if (cs + t + 3 <= D3) {  // dq: W x k2 ; dk2: q x W     ((x cross y)_r = x_{r+1} y_{r+2} - x_{r+2} y_{r+1})
+        v[t + 0] = s * (w[t + 1] * k2v[t + 2] - w[t + 2] * k2v[t + 1]);
+        v[t + 1] = s * (w[t + 2] * k2v[t + 0] - w[t + 0] * k2v[t + 2]);
+        v[t + 2] = s * (w[t + 0] * k2v[t + 1] - w[t + 1] * k2v[t + 0]);
+        ck[t + 0] = s * (qv[t + 1] * w[t + 2] - qv[t + 2] * w[t + 1]);
+        ck[t + 1] = s * (qv[t + 2] * w[t + 0] - qv[t + 0] * w[t + 2]);
+        ck[t + 2] = s * (qv[t + 0] * w[t + 1] - qv[t + 1] * w[t + 0]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 6; ++e) cv[e] = cs + e < D ? dov[e] * __uint_as_float(uu[e]) : 0.f;
+#pragma unroll
+    for (int e = 0; e < 6; e += 2) {
+      *reinterpret_cast<float2*>(&sm.eb.w.ek[r][6 * m + e]) = make_float2(ck[e], ck[e + 1]);
+      *reinterpret_cast<float2*>(&sm.eb.w.ev[r][6 * m + e]) = make_float2(cv[e], cv[e + 1]);
+    }
+  }
+  // reduce-scatter the 8 (six real) dq columns over the 32 lanes, as in q_epilogue_pass32
+#pragma unroll
+  for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+    const bool hi = ln & st;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+    }
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  const int gq = r >> a.lR;
+  const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+  const bool lead = a.R == 32 || ((r >> 5) & 1) == 0;
+  if (act && !lead && (ln & 3) == 0 && col < 6) sm.dqx[gq][6 * m + col] = v[0];
+  if (a.R == 64) named_bar_sync(1, kQNT);
+  if (act && lead && (ln & 3) == 0 && col < 6 && cs + col < D && gq < it.nq) {
+    const float y = a.R == 64 ? v[0] + sm.dqx[gq][6 * m + col] : v[0];
+    const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + col;
+    if (a.out_f32)
+      reinterpret_cast<float*>(a.dq)[off] = y;
+    else
+      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
+  }
+  named_bar_sync(1, kQNT);
+  // key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g); thread -> (sl, column pair)
+  const int P0 = p.np + it.i0;
+  const int nsl = a.R + it.nq - 1;
+  const int npair = (min(24, D - c0) + 1) / 2;
+  for (int idx = tidc; idx < nsl * 12; idx += kQNT) {
+    const int sl = idx / 12, d = 2 * (idx % 12);
+    if (d >= 2 * npair) continue;
+    const int kp = P0 - a.R + 1 + sl;
+    const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
+    float2 xk = make_float2(0.f, 0.f), xv = xk;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int gg = glo + u;
+      if (gg <= ghi) {
+        const int row = (gg << a.lR) + (sl - gg);
+        const float2 tk = *reinterpret_cast<const float2*>(&sm.eb.w.ek[row][d]);
+        const float2 tv = *reinterpret_cast<const float2*>(&sm.eb.w.ev[row][d]);
+        xk.x += tk.x, xk.y += tk.y, xv.x += tv.x, xv.y += tv.y;
+      }
+    }
+    int slot = sbase + sl;
+    if (slot >= a.ring) slot -= a.ring;
+    if (kp >= 0) {
+      float2* ak = reinterpret_cast<float2*>(&sm.acc_k2[slot][c0 + d]);
+      float2* av = reinterpret_cast<float2*>(&sm.acc_v2[slot][c0 + d]);
+      float2 yk = *ak, yv = *av;
+      yk.x += xk.x, yk.y += xk.y, yv.x += xv.x, yv.y += xv.y;
+      *ak = yk;
+      *av = yv;
+    }
+  }
+  named_bar_sync(1, kQNT);
+}
+
 template <int D, bool DET, int RING, bool STAGED>
 __global__ void __launch_bounds__(kQThreads, 1)
     tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
@@ -853,7 +975,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
       mbar_wait(&sm.udone, gc & 1);
       tc_fence_after();
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 5 << 8);
-      if (DET) {
+      if (DET && (a.R == 32 || a.R == 64)) {
+        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 24)
+          q_epilogue_pass_det<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
+      } else if (DET) {
 #pragma unroll 1
         for (int c0 = 0; c0 + 24 <= D; c0 += 24)
           q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256, sub == 0);
