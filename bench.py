@@ -269,6 +269,49 @@ def run_table1(args, c):
         }), flush=True)
 
 
+def run_membound(args, c):
+    """The memory-bound small-window point of SURVEY.md §8(d): windows (32, 8) at config c's shape,
+    MMA intensity w1*w2/3 = 85 flop/B, below the B200 ridge.  Reports achieved HBM GB/s on the
+    algorithmic bytes per (b,h,query row): forward 12*D+4 (q,k,v,k2,v2 read, o written at 2 B/elt,
+    lse fp32), backward 24*D+8 (q,k,v,k2,v2,o,dO read, five gradients written, lse and delta),
+    against the measured HBM copy bandwidth."""
+    import paper_2507_02754_b200 as sa
+    dev = torch.device("cuda", 0)
+    B, H, N, D = (c[k] for k in ("B", "H", "N", "D"))
+    w1, w2 = 32, 8
+    inp = make_inputs(B, N, H, D, seed_of(args.config), dtype="bf16", device="cpu")
+    t = {n: x.to(dev) for n, x in inp.items()}
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(1, args.warmup)):
+        o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2)
+        sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    steps = max(1, args.steps)
+    torch.cuda.synchronize()
+    e[0].record(stream)
+    for _ in range(steps):
+        o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2)
+    e[1].record(stream)
+    for _ in range(steps):
+        sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2)
+    e[2].record(stream)
+    torch.cuda.synchronize()
+    fms, bms = e[0].elapsed_time(e[1]) / steps, e[1].elapsed_time(e[2]) / steps
+    rows = B * H * N
+    fb, bb = rows * (12 * D + 4), rows * (24 * D + 8)
+    pk, src = peaks()
+    cc = dict(c, w1=w1, w2=w2)
+    print(json.dumps({
+        "sweep": "membound", "config": f"B={B} H={H} N={N} D={D} w1={w1} w2={w2} trilinear bf16",
+        "fwd_ms": fms, "bwd_ms": bms, "fwd_gbs": fb / (fms / 1e3) / 1e9, "bwd_gbs": bb / (bms / 1e3) / 1e9,
+        "hbm_peak_gbs": pk["hbm_gbs"], "peak_source": src,
+        "fwd_frac": fb / (fms / 1e3) / 1e9 / pk["hbm_gbs"], "bwd_frac": bb / (bms / 1e3) / 1e9 / pk["hbm_gbs"],
+        "tflops_paper_basis": paper_flops(cc) / ((fms + bms) / 1e3) / 1e12,
+        "paths": {"fwd": {1: "simt", 2: "tcgen05"}.get(sa.fwd_path(B, H, N, D, w1, w2)),
+                  "bwd": {1: "simt", 2: "tcgen05"}.get(sa.bwd_path(B, H, N, D, w1, w2))},
+    }), flush=True)
+
+
 def config_block(c, n, mode="bh"):
     return {"workload": f"{c['name']}: B={c['B']} H={c['H']} N={c['N']} D={c['D']} w1={c['w1']} w2={c['w2']} "
                         f"{'det' if c['det'] else 'trilinear'} {'fwd+bwd' if c['bwd'] else 'fwd'} per GPU",
@@ -291,7 +334,7 @@ def main():
     ap.add_argument("--out-f32", action="store_true", help="write o/grads in fp32 (parity runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep", default=None, choices=["table1"],
+    ap.add_argument("--sweep", default=None, choices=["table1", "membound"],
                     help="table1: the paper's (w1, w2) latency sweep (Table 1, P:335-354) at the chosen "
                          "config's B, H, N, D; one JSON line per pair (not the bench line)")
     ap.add_argument("--mode", default="bh", choices=["bh", "seq"],
@@ -305,6 +348,9 @@ def main():
         return
     if args.sweep == "table1":
         run_table1(args, c)
+        return
+    if args.sweep == "membound":
+        run_membound(args, c)
         return
 
     import paper_2507_02754_b200 as sa
