@@ -508,6 +508,80 @@ __global__ void __launch_bounds__(kThreads, 1)
               reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(v[0] * invL);
           }
         }
+      } else if (a.R < 32 && (a.R & (a.R - 1)) == 0 && a.R >= 2) {
+        // R in {2, 4, 8, 16}: a warp holds 32/R whole queries in aligned groups of R lanes; group
+        // statistics by butterfly shuffles inside the group, the R-row sum of each 16-column block
+        // by a reduce-scatter inside the group (each lane ends with 16/R columns of its query)
+        const bool live = valid && m_ref != -INFINITY;
+        float M = live ? m_ref : -INFINITY;
+        for (int o = a.R >> 1; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float crow = live ? ex2(m_ref - M) : 0.f;
+        float L = live ? l * crow : 0.f;
+        for (int o = a.R >> 1; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        const bool qlive = g < nq;
+        const int gl = lane & (a.R - 1);  // lane within the query's group
+        if (gl == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
+        const float invL = qlive ? 1.f / L : 0.f;
+        const int nf = 16 / a.R;  // columns per lane after the reduce-scatter
+        int cbase = 0;
+        for (int k = 0, st = a.R >> 1; st > 0; ++k, st >>= 1)
+          if (gl & st) cbase += 8 >> k;
+#pragma unroll 1
+        for (int cb = 0; cb < D / 16; ++cb) {
+          uint32_t u[16];
+          tmem_ld16(tU + 16 * cb, u);
+          tmem_ld_wait();
+          float v[16];
+          if (valid) {
+            if (STAGED) {
+              const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
+#pragma unroll
+              for (int t = 0; t < 2; ++t) {
+                const uint4 y = vp[t];
+                const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = bf16x2_to_f2(ys[e]);
+                  v[8 * t + 2 * e] = f.x;
+                  v[8 * t + 2 * e + 1] = f.y;
+                }
+              }
+            } else {
+              load_bf16<16>(v2row + 16 * cb, v);
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] *= crow * __uint_as_float(u[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // stages st = R/2, R/4, ..., 1 with n = 8, 4, 2, 1 kept values
+            const int st = (a.R >> 1) >> k, n = 8 >> k;
+            if (st > 0) {
+              const bool hi = gl & st;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (i < n) {
+                  const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+                  v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                }
+              }
+            }
+          }
+          if (qlive) {
+            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + cbase;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i < nf) {
+                if (a.out_f32)
+                  reinterpret_cast<float*>(a.o)[off + i] = v[i] * invL;
+                else
+                  reinterpret_cast<__nv_bfloat16*>(a.o)[off + i] = __float2bfloat16_rn(v[i] * invL);
+              }
+            }
+          }
+        }
       } else if (a.R == 64) {
         // one query == two warps (lane quarters qd, qd^1): warp-level statistics by shuffles, the
         // partner's partials through shared memory; each warp reduce-scatters its 32 rows, the even

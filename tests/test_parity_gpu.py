@@ -82,6 +82,9 @@ def test_fp32_shapes(B, N, H, D, w1, w2, det):
     (1, 160, 1, 128, 16, 48),    # w2 > w1
     (1, 300, 2, 128, 128, 64),   # R = 64 rows per query (G = 2): the c5 / Table-1 (512, 64) tiling
     (2, 170, 1, 128, 96, 64),    # R = 64, ragged tail
+    (1, 200, 2, 128, 32, 8),     # R = 8 (G = 16): the memory-bound small-window point of §8(d)
+    (1, 96, 1, 64, 20, 4),       # R = 4
+    (1, 70, 1, 128, 10, 2),      # R = 2 (G = 64)
 ])
 def test_bf16_shapes(B, N, H, D, w1, w2, det, force_simt):
     inp = make_inputs(B, N, H, D, seed=7 * N + D, dtype="bf16")
