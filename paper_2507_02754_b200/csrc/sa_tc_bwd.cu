@@ -377,9 +377,6 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
   named_bar_sync(1, kQNT);
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
-#ifdef SA_ABLATE_GATHER
-  if (nsl > 0) return;
-#endif
   // key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g); thread -> (sl, 4 columns)
   for (int idx = tidc; idx < nsl * 8; idx += kQNT) {
     const int sl = idx >> 3, d = 4 * (idx & 7);
@@ -532,9 +529,6 @@ __device__ __forceinline__ void q_epilogue_pass_small(QSmem<D, RING, STAGED>& sm
   named_bar_sync(1, kQNT);
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
-#ifdef SA_ABLATE_GATHER
-  if (nsl > 0) return;
-#endif
   // key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g); thread -> (sl, 4 columns)
   for (int idx = tidc; idx < nsl * 8; idx += kQNT) {
     const int sl = idx >> 3, d = 4 * (idx & 7);
