@@ -1277,7 +1277,7 @@ constexpr int kKVThreads = 32 * (kKVWarpMMA + 1);  // warps 0-7 softmax-gradient
 // TMEM columns: K, V operands (D/2 packed cols each), dV, dK accumulators, 2 x (S^T, dP^T) quarters
 constexpr uint32_t kKK = 0, kKV = 64, kKdV = 128, kKdK = 256, kKSD = 384;
 constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
-constexpr int kKVGmax = 8;    // staged queries per tile
+constexpr int kKVGmax = 16;   // staged queries per tile
 
 struct BwdKVArgs {
   Problem p;  // after the swap: w1 = long window (this kernel's keys), w2 = R
