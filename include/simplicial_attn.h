@@ -158,6 +158,31 @@ sa_status simplicial_attn_bwd_gqa(const void* q, const void* k, const void* v, c
                                   size_t workspace_bytes, int64_t B, int64_t H, int64_t H_kv, int64_t N,
                                   int64_t D, int64_t w1, int64_t w2, uint32_t flags, void* stream);
 
+/* K2_BIAS / V2_BIAS (the paper's kernel listing: the K' and V' tiles get a
+ * scalar added after loading, k2t_tile += K2_BIAS; v2_tile += V2_BIAS).  Computes the same outputs as
+ * simplicial_attn_fwd_gqa / _bwd_gqa run on k2 + k2_bias and v2 + v2_bias, elementwise.  The biased
+ * copies are written into the caller's workspace in the input dtype: bf16 inputs are rounded once
+ * after the add, fp32 inputs are exact.  Because the bias is additive, dk2 and dv2 are also the
+ * gradients with respect to the caller's k2 and v2.  H_kv == H is plain multi-head attention.
+ * Layouts, dtypes, flags, ownership and errors are as for the _gqa entry points.  A workspace
+ * smaller than simplicial_attn_{fwd,bwd}_bias_workspace_bytes(...) -> SA_ERR_WORKSPACE; a NULL
+ * workspace -> SA_ERR_INVALID_ARG.  Enqueued on `stream`; nothing is synchronised. */
+size_t simplicial_attn_fwd_bias_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                                int64_t w1, int64_t w2, uint32_t flags);
+sa_status simplicial_attn_fwd_bias(const void* q, const void* k, const void* v, const void* k2,
+                                   const void* v2, void* o, float* lse, float k2_bias, float v2_bias,
+                                   void* workspace, size_t workspace_bytes, int64_t B, int64_t H,
+                                   int64_t H_kv, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                   uint32_t flags, void* stream);
+size_t simplicial_attn_bwd_bias_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                                int64_t w1, int64_t w2, uint32_t flags);
+sa_status simplicial_attn_bwd_bias(const void* q, const void* k, const void* v, const void* k2,
+                                   const void* v2, const void* o, const float* lse, const void* dO,
+                                   void* dq, void* dk, void* dv, void* dk2, void* dv2, float k2_bias,
+                                   float v2_bias, void* workspace, size_t workspace_bytes, int64_t B,
+                                   int64_t H, int64_t H_kv, int64_t N, int64_t D, int64_t w1,
+                                   int64_t w2, uint32_t flags, void* stream);
+
 /* Which kernel family the dispatcher picks for these arguments (SA_PATH_*), 0 if unsupported. */
 int simplicial_attn_fwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
                              uint32_t flags);

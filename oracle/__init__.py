@@ -21,6 +21,13 @@ forward_gqa(q, k, v, k2, v2, w1, w2, det=False) / backward_gqa(...)
     key heads are repeated to H and the plain oracle runs; each key-side gradient
     is the sum of the gradients of the query heads that share it (chain rule).
 
+forward_bias(q, k, v, k2, v2, w1, w2, k2_bias, v2_bias, det=False) / backward_bias(...)
+    K2_BIAS / V2_BIAS of the paper's kernel listing: after loading,
+    ``k2t_tile += K2_BIAS; v2_tile += V2_BIAS``, i.e. the method runs on
+    K' + b and V' + b'.  Written as that: the scalars are added in float64 and the
+    (grouped-query) oracle runs on the shifted tensors; the gradients with respect to
+    K' and V' are those with respect to the shifted tensors (d(x + b)/dx = 1).
+
 All arrays are float64 numpy arrays; q/dO are [B, N, H, D], key-side tensors
 are [B, n_prefix+N, H, D] (query row i sits at key position n_prefix+i).
 """
@@ -138,3 +145,13 @@ def backward_gqa(q, k, v, k2, v2, dO, w1, w2, det=False):
     r = q.shape[2] // Hk
     dq, *gk = backward(q, *(_repeat_heads(t, r) for t in (k, v, k2, v2)), dO, w1, w2, det=det)
     return (dq, *(g.reshape(B, NK, Hk, r, D).sum(axis=3) for g in gk))
+
+
+def forward_bias(q, k, v, k2, v2, w1, w2, k2_bias, v2_bias, det=False):
+    k2, v2 = _f64(k2), _f64(v2)
+    return forward_gqa(q, k, v, k2 + float(k2_bias), v2 + float(v2_bias), w1, w2, det=det)
+
+
+def backward_bias(q, k, v, k2, v2, dO, w1, w2, k2_bias, v2_bias, det=False):
+    k2, v2 = _f64(k2), _f64(v2)
+    return backward_gqa(q, k, v, k2 + float(k2_bias), v2 + float(v2_bias), dO, w1, w2, det=det)

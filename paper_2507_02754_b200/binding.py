@@ -32,6 +32,8 @@ EXPORTS = (
     "simplicial_attn_profile_enable", "simplicial_attn_profile_read",
     "simplicial_attn_fwd_gqa_workspace_bytes", "simplicial_attn_fwd_gqa",
     "simplicial_attn_bwd_gqa_workspace_bytes", "simplicial_attn_bwd_gqa",
+    "simplicial_attn_fwd_bias_workspace_bytes", "simplicial_attn_fwd_bias",
+    "simplicial_attn_bwd_bias_workspace_bytes", "simplicial_attn_bwd_bias",
 )
 
 _lib = None
@@ -50,7 +52,7 @@ def load_library(build: bool = True):
     if not os.path.exists(path):
         raise SimplicialAttnError(f"libsimplicial.so missing at {path}; run __graft_entry__.build()")
     lib = ctypes.CDLL(path)
-    P, I, U, S = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
+    P, I, U, S, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t, ctypes.c_float
     sig = {
         "simplicial_attn_fwd": ([P] * 7 + [I] * 6 + [U, P], ctypes.c_int),
         "simplicial_attn_fwd_prefixed": ([P] * 7 + [I] * 7 + [U, P], ctypes.c_int),
@@ -74,6 +76,10 @@ def load_library(build: bool = True):
         "simplicial_attn_fwd_gqa": ([P] * 8 + [S] + [I] * 7 + [U, P], ctypes.c_int),
         "simplicial_attn_bwd_gqa_workspace_bytes": ([I] * 7 + [U], S),
         "simplicial_attn_bwd_gqa": ([P] * 14 + [S] + [I] * 7 + [U, P], ctypes.c_int),
+        "simplicial_attn_fwd_bias_workspace_bytes": ([I] * 7 + [U], S),
+        "simplicial_attn_fwd_bias": ([P] * 7 + [F, F, P, S] + [I] * 7 + [U, P], ctypes.c_int),
+        "simplicial_attn_bwd_bias_workspace_bytes": ([I] * 7 + [U], S),
+        "simplicial_attn_bwd_bias": ([P] * 13 + [F, F, P, S] + [I] * 7 + [U, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -146,15 +152,27 @@ def _workspace(device, nbytes: int, kind: str = "fwd") -> torch.Tensor:
 
 
 def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool = False,
-            n_prefix: int = 0, force_simt: bool = False):
+            n_prefix: int = 0, force_simt: bool = False, k2_bias: float = 0.0, v2_bias: float = 0.0):
     """o, lse = 2-simplicial attention forward (simplicial_attn_fwd_prefixed; key-side tensors with
-    fewer heads than q -> grouped-query simplicial_attn_fwd_gqa)."""
+    fewer heads than q -> grouped-query simplicial_attn_fwd_gqa; a nonzero k2_bias / v2_bias ->
+    simplicial_attn_fwd_bias)."""
     h_kv = k.shape[2] if k.dim() == 4 and k.shape[2] != q.shape[2] else None
     B, N, H, D = _check_inputs(q, (k, v, k2, v2), n_prefix, h_kv)
     L = lib()
     flags = _flags(q.dtype, det, out_f32, force_simt)
     o = torch.empty((B, N, H, D), dtype=_out_dtype(flags), device=q.device)
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device)
+    if k2_bias != 0.0 or v2_bias != 0.0:
+        if n_prefix:
+            raise SimplicialAttnError("the bias entry points take no key prefix")
+        hk = h_kv or H
+        wsb = int(L.simplicial_attn_fwd_bias_workspace_bytes(B, H, hk, N, D, w1, w2, flags))
+        ws = _workspace(q.device, wsb, "fwd_bias")
+        st = L.simplicial_attn_fwd_bias(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
+                                        float(k2_bias), float(v2_bias), _ptr(ws), ws.numel(), B, H, hk, N, D,
+                                        w1, w2, flags, _stream(q.device))
+        _check(st, "simplicial_attn_fwd_bias")
+        return o, lse
     if h_kv is not None:
         if n_prefix:
             raise SimplicialAttnError("grouped-query mode takes no key prefix")
@@ -173,9 +191,11 @@ def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool 
 
 
 def backward(q, k, v, k2, v2, o, lse, dO, w1: int, w2: int, det: bool = False, out_f32: bool = False,
-             n_prefix: int = 0, force_simt: bool = False, workspace: torch.Tensor | None = None):
+             n_prefix: int = 0, force_simt: bool = False, workspace: torch.Tensor | None = None,
+             k2_bias: float = 0.0, v2_bias: float = 0.0):
     """dq, dk, dv, dk2, dv2 = 2-simplicial attention backward (simplicial_attn_bwd_prefixed; key-side
-    tensors with fewer heads than q -> grouped-query simplicial_attn_bwd_gqa)."""
+    tensors with fewer heads than q -> grouped-query simplicial_attn_bwd_gqa; a nonzero k2_bias /
+    v2_bias -> simplicial_attn_bwd_bias)."""
     h_kv = k.shape[2] if k.dim() == 4 and k.shape[2] != q.shape[2] else None
     B, N, H, D = _check_inputs(q, (k, v, k2, v2), n_prefix, h_kv)
     L = lib()
@@ -185,6 +205,18 @@ def backward(q, k, v, k2, v2, o, lse, dO, w1: int, w2: int, det: bool = False, o
         raise SimplicialAttnError("o must be in the output dtype and dO in the input dtype, contiguous")
     dq = torch.empty((B, N, H, D), dtype=od, device=q.device)
     dk, dv, dk2, dv2 = (torch.empty_like(k, dtype=od) for _ in range(4))
+    if k2_bias != 0.0 or v2_bias != 0.0:
+        if n_prefix:
+            raise SimplicialAttnError("the bias entry points take no key prefix")
+        hk = h_kv or H
+        wsb = int(L.simplicial_attn_bwd_bias_workspace_bytes(B, H, hk, N, D, w1, w2, flags))
+        ws = _workspace(q.device, wsb, "bwd_bias")
+        st = L.simplicial_attn_bwd_bias(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
+                                        _ptr(dO), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dk2), _ptr(dv2),
+                                        float(k2_bias), float(v2_bias), _ptr(ws), ws.numel(), B, H, hk, N, D,
+                                        w1, w2, flags, _stream(q.device))
+        _check(st, "simplicial_attn_bwd_bias")
+        return dq, dk, dv, dk2, dv2
     if h_kv is not None:
         if n_prefix:
             raise SimplicialAttnError("grouped-query mode takes no key prefix")

@@ -122,6 +122,8 @@ cudaError_t gqa_reduce(const float* part, void* out, bool out_f32, int64_t rows,
                        cudaStream_t st);
 cudaError_t cast_f32_bf16(const float* a, void* b, int64_t n, cudaStream_t st);
 cudaError_t cast_bf16_f32(const void* a, float* b, int64_t n, cudaStream_t st);
+cudaError_t add_bias(const void* k2, const void* v2, void* k2b, void* v2b, int64_t n, bool f32, float b2k,
+                     float b2v, cudaStream_t st);
 
 static bool use_tc_fwd(const Problem& p, uint32_t flags) {
   if (flags & (SA_IN_F32 | SA_FORCE_SIMT)) return false;
@@ -571,6 +573,79 @@ sa_status simplicial_attn_bwd_gqa(const void* q, const void* k, const void* v, c
     e = gqa_reduce(part[t], outs[t], out_f32, int64_t(p.B) * p.NK(), p.Hk, p.H / p.Hk, p.D, st);
   if (e == cudaSuccess && !out_f32) e = cast_f32_bf16(dq32, dq, nq, st);
   return cuda_status(e);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// K2_BIAS / V2_BIAS: the entry points add the two
+// scalars to K' and V' into workspace copies, then run the grouped-query entry points (H_kv == H is
+// plain multi-head) on the copies.  The bias is additive, so the gradients with respect to the
+// biased copies are the gradients with respect to the caller's K' and V'.
+// workspace: [k2 + b] [v2 + b] (input dtype, [B, N, H_kv, D] each) [the inner call's workspace]
+namespace sa {
+static size_t bias_copy_bytes(const Problem& p, uint32_t flags) {
+  const size_t es = (flags & SA_IN_F32) ? 4 : 2;
+  return align256(size_t(p.B) * p.NK() * p.Hk * p.D * es);
+}
+}  // namespace sa
+
+extern "C" {
+
+size_t simplicial_attn_fwd_bias_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                                int64_t w1, int64_t w2, uint32_t flags) {
+  Problem p;
+  if (make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p) != SA_OK) return 0;
+  return 2 * bias_copy_bytes(p, flags) + simplicial_attn_fwd_gqa_workspace_bytes(B, H, H_kv, N, D, w1, w2, flags);
+}
+
+sa_status simplicial_attn_fwd_bias(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                                   void* o, float* lse, float k2_bias, float v2_bias, void* workspace,
+                                   size_t workspace_bytes, int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                   int64_t w1, int64_t w2, uint32_t flags, void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse || !workspace) return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p);
+  if (s != SA_OK) return s;
+  if (workspace_bytes < simplicial_attn_fwd_bias_workspace_bytes(B, H, H_kv, N, D, w1, w2, flags))
+    return SA_ERR_WORKSPACE;
+  const size_t cb = bias_copy_bytes(p, flags);
+  char* w = (char*)workspace;
+  cudaGetLastError();
+  cudaError_t e = add_bias(k2, v2, w, w + cb, int64_t(p.B) * p.NK() * p.Hk * p.D, (flags & SA_IN_F32) != 0,
+                           k2_bias, v2_bias, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  return simplicial_attn_fwd_gqa(q, k, v, w, w + cb, o, lse, w + 2 * cb, workspace_bytes - 2 * cb, B, H, H_kv, N,
+                                 D, w1, w2, flags, stream);
+}
+
+size_t simplicial_attn_bwd_bias_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                                int64_t w1, int64_t w2, uint32_t flags) {
+  Problem p;
+  if (make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p) != SA_OK) return 0;
+  return 2 * bias_copy_bytes(p, flags) + simplicial_attn_bwd_gqa_workspace_bytes(B, H, H_kv, N, D, w1, w2, flags);
+}
+
+sa_status simplicial_attn_bwd_bias(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                                   const void* o, const float* lse, const void* dO, void* dq, void* dk, void* dv,
+                                   void* dk2, void* dv2, float k2_bias, float v2_bias, void* workspace,
+                                   size_t workspace_bytes, int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
+                                   int64_t w1, int64_t w2, uint32_t flags, void* stream) {
+  if (!q || !k || !v || !k2 || !v2 || !o || !lse || !dO || !dq || !dk || !dv || !dk2 || !dv2 || !workspace)
+    return SA_ERR_INVALID_ARG;
+  Problem p;
+  sa_status s = make_problem_gqa(B, H, H_kv, N, D, w1, w2, flags, &p);
+  if (s != SA_OK) return s;
+  if (workspace_bytes < simplicial_attn_bwd_bias_workspace_bytes(B, H, H_kv, N, D, w1, w2, flags))
+    return SA_ERR_WORKSPACE;
+  const size_t cb = bias_copy_bytes(p, flags);
+  char* w = (char*)workspace;
+  cudaGetLastError();
+  cudaError_t e = add_bias(k2, v2, w, w + cb, int64_t(p.B) * p.NK() * p.Hk * p.D, (flags & SA_IN_F32) != 0,
+                           k2_bias, v2_bias, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  return simplicial_attn_bwd_gqa(q, k, v, w, w + cb, o, lse, dO, dq, dk, dv, dk2, dv2, w + 2 * cb,
+                                 workspace_bytes - 2 * cb, B, H, H_kv, N, D, w1, w2, flags, stream);
 }
 
 }  // extern "C"

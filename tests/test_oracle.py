@@ -365,3 +365,49 @@ def test_gqa_against_autograd(oracle_mod, H, Hk, det):
     assert np.max(np.abs(o - ro.detach().numpy())) < 1e-12
     for g, t in zip(grads, [tq, *tk]):
         assert np.max(np.abs(g - t.grad.numpy())) < 1e-10
+
+
+@pytest.mark.parametrize("w1,w2", [(5, 3), (3, 16)])
+def test_bias_collapse_to_dot_attention(oracle_mod, w1, w2):
+    """K2_BIAS / V2_BIAS on K' = V' = 0 with both biases 1: the shifted K', V' are all
+    ones, so the output is sliding-window dot-product attention over (Q, K, V), computed by torch
+    SDPA, and lse shifts by ln(min(i+1, w2)) (reading R19).  A bias added to the wrong operand (K or
+    V instead of K' or V') fails this."""
+    B, N, H, D = 1, 20, 2, 8
+    q, k, v, _, _, _ = rand_problem(B, N, H, D, seed=11)
+    zeros = np.zeros_like(k)
+    o, lse = oracle_mod.forward_bias(q, k, v, zeros, zeros, w1, w2, 1.0, 1.0)
+    tq, tk, tv = (torch.from_numpy(x).permute(0, 2, 1, 3) for x in (q, k, v))
+    i = torch.arange(N)[:, None]
+    j = torch.arange(N)[None, :]
+    mask = (j <= i) & (j > i - w1)
+    ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, attn_mask=mask)
+    np.testing.assert_allclose(o, ref.permute(0, 2, 1, 3).numpy(), rtol=0, atol=1e-12)
+    sc = (tq @ tk.transpose(-1, -2)) / math.sqrt(D)
+    lse_dot = torch.logsumexp(sc.masked_fill(~mask, float("-inf")), dim=-1).numpy()
+    shift = np.log(np.minimum(np.arange(N) + 1, w2))
+    np.testing.assert_allclose(lse, lse_dot + shift, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("H,Hk,det", [(2, 2, False), (4, 2, True)])
+def test_bias_against_autograd(oracle_mod, H, Hk, det):
+    """forward_bias / backward_bias against torch autograd of the dense Alg. 1 model fed K' + b and
+    V' + b': autograd differentiates through the add, so its K'/V' gradients are with
+    respect to the caller's unshifted tensors."""
+    B, N, D, w1, w2 = 1, 9, 6, 4, 3
+    b2k, b2v = 0.37, -1.25
+    rng = np.random.default_rng(H * 7 + Hk)
+    q = rng.standard_normal((B, N, H, D))
+    dO = rng.standard_normal((B, N, H, D))
+    keys = [rng.standard_normal((B, N, Hk, D)) for _ in range(4)]
+    o, _ = oracle_mod.forward_bias(q, *keys, w1, w2, b2k, b2v, det=det)
+    grads = oracle_mod.backward_bias(q, *keys, dO, w1, w2, b2k, b2v, det=det)
+    tq = torch.tensor(q, requires_grad=True)
+    tk = [torch.tensor(x, requires_grad=True) for x in keys]
+    sh = [tk[0], tk[1], tk[2] + b2k, tk[3] + b2v]
+    exp = [t.repeat_interleave(H // Hk, dim=2) for t in sh]
+    ro = dense_torch(tq, *exp, w1, w2, det=det)
+    ro.backward(torch.tensor(dO))
+    assert np.max(np.abs(o - ro.detach().numpy())) < 1e-12
+    for g, t in zip(grads, [tq, *tk]):
+        assert np.max(np.abs(g - t.grad.numpy())) < 1e-10

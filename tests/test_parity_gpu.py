@@ -268,3 +268,48 @@ def test_gqa(dtype, tol, H, Hk, D, w1, w2, det):
         g16 = sa.backward(*t[:5], o16, lse16, t[5], w1, w2, det=det)
         assert all(x.dtype == (torch.bfloat16 if dtype == "bf16" else torch.float32) for x in g16)
         assert maxabs(g16[1], rg[1]) <= 4 * TOL_BF16
+
+
+@pytest.mark.parametrize("dtype,tol", [("bf16", TOL_BF16), ("f32", TOL_F32)])
+@pytest.mark.parametrize("H,Hk,D,w1,w2,det", [
+    (2, 2, 128, 96, 32, False),   # multi-head, tcgen05 path
+    (4, 2, 64, 64, 16, True),     # grouped-query, determinant
+])
+def test_bias(dtype, tol, H, Hk, D, w1, w2, det):
+    """K2_BIAS / V2_BIAS entry points against the oracle's forward_bias / backward_bias
+    (float64 add of the scalars, then the method); also through the autograd wrapper."""
+    B, N = 2, 160
+    b2k, b2v = 0.37, -1.25
+    g = torch.Generator().manual_seed(H * 10 + D)
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q, dO = (torch.randn(B, N, H, D, generator=g).to(dt) for _ in range(2))
+    keys = [torch.randn(B, N, Hk, D, generator=g).to(dt) for _ in range(4)]
+    t = [x.to(DEV) for x in (q, *keys, dO)]
+    o, lse = sa.forward(*t[:5], w1, w2, det=det, out_f32=True, k2_bias=b2k, v2_bias=b2v)
+    grads = sa.backward(*t[:5], o, lse, t[5], w1, w2, det=det, out_f32=True, k2_bias=b2k, v2_bias=b2v)
+    torch.cuda.synchronize()
+    a = [f64(x) for x in (q, *keys, dO)]
+    if dtype == "bf16":
+        # the paper casts k2 + K2_BIAS to the GEMM dtype bf16 (P:791-794); the bias entry points also
+        # round v2 + V2_BIAS to bf16 (reading R14): the oracle gets the same rounded shifted rows
+        # (fp32 add, round to nearest even), passed with zero bias
+        sk2, sv2 = ((x.float() + b).to(torch.bfloat16) for x, b in ((keys[2], b2k), (keys[3], b2v)))
+        ab, bk, bv = [*a[:3], f64(sk2), f64(sv2)], 0.0, 0.0
+    else:
+        ab, bk, bv = a[:5], b2k, b2v
+    ro, rl = oracle.forward_bias(*ab, w1, w2, bk, bv, det=det)
+    rg = oracle.backward_bias(*ab, a[5], w1, w2, bk, bv, det=det)
+    got = dict(zip(("o", "lse", "dq", "dk", "dv", "dk2", "dv2"), (o, lse, *grads)))
+    ref = dict(zip(("o", "lse", "dq", "dk", "dv", "dk2", "dv2"), (ro, rl, *rg)))
+    assert_close(got, ref, tol)
+    # the caller's k2 / v2 are untouched (the biased copies live in the workspace)
+    assert torch.equal(t[3].cpu(), keys[2]) and torch.equal(t[4].cpu(), keys[3])
+    if Hk == H:
+        leaves = [x.clone().requires_grad_(True) for x in t[:5]]
+        oa = sa_pkg.simplicial_attention(*leaves, w1, w2, det=det, k2_bias=b2k, v2_bias=b2v)
+        oa.backward(t[5])
+        o_d, lse_d = sa.forward(*t[:5], w1, w2, det=det, k2_bias=b2k, v2_bias=b2v)
+        g_d = sa.backward(*t[:5], o_d, lse_d, t[5], w1, w2, det=det, k2_bias=b2k, v2_bias=b2v)
+        assert torch.equal(oa, o_d)
+        for lf, gd in zip(leaves, g_d):
+            assert torch.equal(lf.grad, gd)
