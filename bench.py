@@ -256,6 +256,14 @@ def run_table1(args, c):
             fms += e[0].elapsed_time(e[1])
             bms += e[1].elapsed_time(e[2])
         fms, bms = fms / steps, bms / steps
+        # per-kernel split of one more fwd+bwd (library CUDA-event profiling)
+        sa.profile_read()
+        sa.profile_enable(True)
+        o, lse = fwd()
+        bwd(o, lse)
+        torch.cuda.synchronize()
+        kern = {n: round(v[0], 3) for n, v in sa.profile_read().items()}
+        sa.profile_enable(False)
         fl = paper_flops(cc)
         print(json.dumps({
             "sweep": "table1", "w1": w1, "w2": w2, "w1xw2": w1 * w2,
@@ -265,6 +273,7 @@ def run_table1(args, c):
             "fwd_tflops": paper_flops(cc, ("fwd",)) / (fms / 1e3) / 1e12,
             "paths": {"fwd": {1: "simt", 2: "tcgen05"}.get(sa.fwd_path(B, H, N, D, w1, w2, det=det)),
                       "bwd": {1: "simt", 2: "tcgen05"}.get(sa.bwd_path(B, H, N, D, w1, w2, det=det))},
+            "kernels_ms": kern,
             "paper_latency_ms": paper_ms, "paper_note": "paper's shape/hardware unstated (P:335-354); context only",
         }), flush=True)
 

@@ -35,8 +35,8 @@ namespace {
 using namespace tc;
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kMaxR = 64;  // bwd_q: rows per query (folded window w2) supported by the ring
-constexpr int kRingMax = 66;
+constexpr int kMaxR = 128;  // bwd_q: rows per query (folded window w2) supported
+constexpr int kRingMax = 66;  // larger rings (R = 128) live in a global per-CTA slab (L2-resident)
 
 
 // ------------------------------------------------------------------------------------------
@@ -78,34 +78,54 @@ struct BwdQArgs {
   const float *lse, *delta;
   void *dq, *dk2, *dv2;
   float* band;  // [grid][2 start/end][2 k2/v2][R-1][D]
+  float* gring;  // R = 128 determinant: [grid][2 k2/v2][ring][D] fp32 ring, each CTA's own (no atomics)
   int out_f32, R, lR, G, ngroups, items, per_cta, ring;
 };
 
 template <int D, int RING, bool STAGED>
 struct QSmem {
-  static constexpr int kStages = 3;
+  // RING variants: <= kRingMax shared-memory ring (R <= 64); 129: R = 128 determinant, ring in the
+  // global slab BwdQArgs::gring (generic passes); 130: R = 128 trilinear (G = 1), ring in shared
+  // memory with a padded pitch (row-owned updates, q_epilogue_g1), two K/V stages to make room
+  static constexpr bool kGR = RING == 129;
+  static constexpr bool kG1 = RING == 130;
+  static constexpr int kStages = kG1 ? 2 : 3;
   static constexpr int kPanelBytes = kQChunk * 128;
   static constexpr int kStageBytes = kQChunk * D * 2;
+  static constexpr int kAP = kG1 ? D + 4 : D;  // ring pitch (floats)
+  static constexpr int kEB = kG1 ? 1 : 128;    // eb rows (unused by the G = 1 pass)
   alignas(1024) uint8_t k[kStages][kStageBytes];
   alignas(1024) uint8_t v[kStages][kStageBytes];
-  float acc_k2[RING][D];
-  float acc_v2[RING][D];
+  alignas(16) float acc_k2[kGR ? 1 : RING][kAP];
+  alignas(16) float acc_v2[kGR ? 1 : RING][kAP];
   alignas(16) union {
     struct {
-      float eq[128][25], ek[128][25], ev[128][25];
+      float eq[kEB][25], ek[kEB][25], ev[kEB][25];
     } g;  // generic passes (PW <= 24)
     struct {
-      float ek[128][36], ev[128][36];  // 16-byte aligned rows (float4 traffic, conflict-free)
+      float ek[kEB][36], ev[kEB][36];  // 16-byte aligned rows (float4 traffic, conflict-free)
     } w;  // R = 32 trilinear passes (PW = 32, dq reduced in registers)
   } eb;
   // staged rows; pitch D+8 halves so that lanes reading consecutive rows hit distinct banks
   alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D + 8];
   float slse[2][16], sdl[2][16];
   float dqx[2][32];  // R = 64: the odd lane quarter's dq column partials of the current pass
+  float dq4[kG1 ? 4 : 1][D];  // R = 128 trilinear: per-lane-quarter dq partials
   uint64_t kvfull[kStages], kvempty[kStages];
   uint64_t sfull[2], pready[2], udone, aready;
   uint32_t tmem_base;
 };
+
+// dK2 / dV2 accumulator ring rows (which = 0: k2, 1: v2): shared memory, or the CTA's global slab
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ auto q_acc(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, int which) {
+  using Sm = QSmem<D, RING, STAGED>;
+  using Row = float(*)[Sm::kAP];
+  if constexpr (Sm::kGR)
+    return reinterpret_cast<Row>(a.gring + (size_t(blockIdx.x) * 2 + which) * size_t(a.ring) * D);
+  else
+    return which ? static_cast<Row>(sm.acc_v2) : static_cast<Row>(sm.acc_k2);
+}
 
 struct QItem {
   int bh, b, h, hk, grp, i0, nq, jbeg, span, nch;  // hk: the key head query head h reads (GQA)
@@ -303,8 +323,8 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
     }
     int slot = sbase + sl;  // (P0 - R + 1 + sl) mod ring
     if (slot >= a.ring) slot -= a.ring;
-    sm.acc_k2[slot][c0 + d] += xk;
-    sm.acc_v2[slot][c0 + d] += xv;
+    q_acc(sm, a, 0)[slot][c0 + d] += xk;
+    q_acc(sm, a, 1)[slot][c0 + d] += xv;
   }
   named_bar_sync(1, kQNT);
 }
@@ -396,8 +416,8 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
     if (kp >= 0) {
-      float4* ak = reinterpret_cast<float4*>(&sm.acc_k2[slot][c0 + d]);
-      float4* av = reinterpret_cast<float4*>(&sm.acc_v2[slot][c0 + d]);
+      float4* ak = reinterpret_cast<float4*>(&q_acc(sm, a, 0)[slot][c0 + d]);
+      float4* av = reinterpret_cast<float4*>(&q_acc(sm, a, 1)[slot][c0 + d]);
       float4 xk = *ak, xv = *av;
       xk.x += (tk[0].x + tk[1].x) + (tk[2].x + tk[3].x);
       xk.y += (tk[0].y + tk[1].y) + (tk[2].y + tk[3].y);
@@ -412,6 +432,77 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
     }
   }
   named_bar_sync(1, kQNT);
+}
+
+// R = 128 trilinear (G = 1): the tile is one query's 128 rows (row r = kk, key row kpos = P0-127+r).
+// Warp m = 2 half + sub of a lane quarter takes columns c0+8m..+8 of W and U for its 32 rows.  Each
+// row has its own key row, so dK2/dV2 need no cross-row reduction: the thread adds its row's
+// s q o W and dO o U straight into the ring (padded pitch: float4 traffic conflict-free).  dq is a
+// register reduce-scatter over the 32 lanes into per-lane-quarter partials (dq4), summed by the
+// caller after one barrier.  No barrier inside the pass.
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_g1(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, int c0, int half,
+                                              int sub, int r, bool valid, const QRows& rw, uint32_t tW, uint32_t tU,
+                                              int sbase) {
+  const float s = a.p.scale;
+  const int ln = r & 31;
+  const int m = 2 * half + sub;
+  const int cs = c0 + 8 * m;
+  uint32_t uw[8], uu[8];
+  tmem_ld8(tW + cs, uw);
+  tmem_ld8(tU + cs, uu);
+  float k2v[8], qv[8], dov[8];
+  if (valid) {
+    load_f16<8>(rw.k2 + cs, k2v);
+    load_f16<8>(rw.q + cs, qv);
+    load_f16<8>(rw.dO + cs, dov);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
+  }
+  int slot = sbase + r;
+  if (slot >= a.ring) slot -= a.ring;
+  auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
+  float4 xk0 = make_float4(0.f, 0.f, 0.f, 0.f), xk1 = xk0, xv0 = xk0, xv1 = xk0;
+  if (valid) {
+    xk0 = *reinterpret_cast<const float4*>(&ak[slot][cs]);
+    xk1 = *reinterpret_cast<const float4*>(&ak[slot][cs + 4]);
+    xv0 = *reinterpret_cast<const float4*>(&av[slot][cs]);
+    xv1 = *reinterpret_cast<const float4*>(&av[slot][cs + 4]);
+  }
+  tmem_ld_wait();
+  float v[8], ck[8], cv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float w = __uint_as_float(uw[e]);
+    v[e] = s * k2v[e] * w;
+    ck[e] = s * qv[e] * w;
+    cv[e] = dov[e] * __uint_as_float(uu[e]);
+  }
+  if (valid) {
+    *reinterpret_cast<float4*>(&ak[slot][cs]) =
+        make_float4(xk0.x + ck[0], xk0.y + ck[1], xk0.z + ck[2], xk0.w + ck[3]);
+    *reinterpret_cast<float4*>(&ak[slot][cs + 4]) =
+        make_float4(xk1.x + ck[4], xk1.y + ck[5], xk1.z + ck[6], xk1.w + ck[7]);
+    *reinterpret_cast<float4*>(&av[slot][cs]) =
+        make_float4(xv0.x + cv[0], xv0.y + cv[1], xv0.z + cv[2], xv0.w + cv[3]);
+    *reinterpret_cast<float4*>(&av[slot][cs + 4]) =
+        make_float4(xv1.x + cv[4], xv1.y + cv[5], xv1.z + cv[6], xv1.w + cv[7]);
+  }
+  // reduce-scatter the 8 columns over the 32 lanes (as in q_epilogue_pass32)
+#pragma unroll
+  for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+    const bool hi = ln & st;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+    }
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+  if ((ln & 3) == 0) sm.dq4[r >> 5][cs + col] = v[0];
 }
 
 // Determinant pass over 24 columns [c0, c0+24) (eight 3-chunks), R in {32, 64}: warp m = 2 half + sub
@@ -567,8 +658,8 @@ __device__ __forceinline__ void q_epilogue_pass_small(QSmem<D, RING, STAGED>& sm
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
     if (kp >= 0) {
-      float4* ak = reinterpret_cast<float4*>(&sm.acc_k2[slot][c0 + d]);
-      float4* av = reinterpret_cast<float4*>(&sm.acc_v2[slot][c0 + d]);
+      float4* ak = reinterpret_cast<float4*>(&q_acc(sm, a, 0)[slot][c0 + d]);
+      float4* av = reinterpret_cast<float4*>(&q_acc(sm, a, 1)[slot][c0 + d]);
       float4 xk = *ak, xv = *av;
       xk.x += sk.x, xk.y += sk.y, xk.z += sk.z, xk.w += sk.w;
       xv.x += sv4.x, xv.y += sv4.y, xv.z += sv4.z, xv.w += sv4.w;
@@ -690,8 +781,8 @@ __device__ __forceinline__ void q_epilogue_pass_det(QSmem<D, RING, STAGED>& sm, 
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
     if (kp >= 0) {
-      float2* ak = reinterpret_cast<float2*>(&sm.acc_k2[slot][c0 + d]);
-      float2* av = reinterpret_cast<float2*>(&sm.acc_v2[slot][c0 + d]);
+      float2* ak = reinterpret_cast<float2*>(&q_acc(sm, a, 0)[slot][c0 + d]);
+      float2* av = reinterpret_cast<float2*>(&q_acc(sm, a, 1)[slot][c0 + d]);
       float2 yk = *ak, yv = *av;
       yk.x += xk.x, yk.y += xk.y, yv.x += xv.x, yv.y += xv.y;
       *ak = yk;
@@ -732,9 +823,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
     fence_mbar_init();
   }
   if (warp == kQWarpMMA) tmem_alloc<512>(&sm.tmem_base);
-  for (int e = threadIdx.x; e < RING * D; e += kQThreads) {
-    (&sm.acc_k2[0][0])[e] = 0.f;
-    (&sm.acc_v2[0][0])[e] = 0.f;
+  for (int e = threadIdx.x; e < a.ring * Sm::kAP; e += kQThreads) {
+    (&q_acc(sm, a, 0)[0][0])[e] = 0.f;
+    (&q_acc(sm, a, 1)[0][0])[e] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -1137,7 +1228,21 @@ __global__ void __launch_bounds__(kQThreads, 1)
       mbar_wait(&sm.udone, gc & 1);
       tc_fence_after();
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 5 << 8);
-      if (DET && (a.R == 32 || a.R == 64)) {
+      if constexpr (Sm::kG1) {
+        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 32)
+          q_epilogue_g1<D, RING, STAGED>(sm, a, c0, half, sub, r, valid, rw, tW, tU, sbase);
+        named_bar_sync(1, kQNT);
+        if (tid256 < D && it.nq > 0) {
+          const float y = (sm.dq4[0][tid256] + sm.dq4[1][tid256]) + (sm.dq4[2][tid256] + sm.dq4[3][tid256]);
+          const int64_t off = p.qoff(it.b, it.i0, it.h) + tid256;
+          if (a.out_f32)
+            reinterpret_cast<float*>(a.dq)[off] = y;
+          else
+            reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
+        }
+      } else if (DET && (a.R == 32 || a.R == 64)) {
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 24)
@@ -1181,9 +1286,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
         if (kp < 0 || kp >= p.NK()) continue;
         int slot = fbase + idx / D;
         if (slot >= a.ring) slot -= a.ring;
-        const float vk = sm.acc_k2[slot][d], vv = sm.acc_v2[slot][d];
-        sm.acc_k2[slot][d] = 0.f;
-        sm.acc_v2[slot][d] = 0.f;
+        const float vk = q_acc(sm, a, 0)[slot][d], vv = q_acc(sm, a, 1)[slot][d];
+        q_acc(sm, a, 0)[slot][d] = 0.f;
+        q_acc(sm, a, 1)[slot][d] = 0.f;
         if (start_open && kp < PS) {
           float* bnd = a.band + ((size_t(blockIdx.x) * 2 + 0) * 2) * (a.R - 1) * D;
           const int rr = kp - (PS - a.R + 1);
@@ -1957,13 +2062,16 @@ static bool swapped(const Problem& p) { return p.w1 < p.w2; }
 bool tc_bwd_supported(const Problem& p) {
   const int R = swapped(p) ? p.w1 : p.w2;
   if (!(p.D == 64 || p.D == 128)) return false;
-  if (R < 2 || R > kMaxR || (R & (R - 1))) return false;  // power-of-two rows per query
-  const int G = 128 / R;
-  return R + G <= kRingMax;
+  return R >= 2 && R <= kMaxR && (R & (R - 1)) == 0;  // power-of-two rows per query
 }
 
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
+static int q_grid(const Problem& p, int R, int G, int* per_cta, int* items_out);
+static int q_grid_n(const Problem& p, int R, int G) {
+  int pc, items;
+  return q_grid(p, R, G, &pc, &items);
+}
 static int q_grid(const Problem& p, int R, int G, int* per_cta, int* items_out) {
   const int ngroups = (p.N + G - 1) / G;
   const int items = ngroups * p.B * p.H;
@@ -1985,7 +2093,8 @@ size_t tc_bwd_workspace_bytes(const Problem& p0) {
   const int grid = q_grid(p, R, G, &pc, &items);
   const size_t n = p.nkey(), nq = size_t(p.B) * p.N * p.H * p.D;
   return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 4 * a256(n * 2) + 2 * a256(nq * 2) +
-         a256(sizeof(float) * size_t(grid) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
+         a256(sizeof(float) * size_t(grid) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D) +
+         (R + G > kRingMax && p.det ? a256(sizeof(float) * size_t(grid) * 2 * (R + G) * p.D) : 0);
 }
 
 cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const void* k, const void* v, const void* k2,
@@ -2020,6 +2129,8 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   char* dof = w;
   w += a256(nq * 2);
   float* band = (float*)w;
+  w += a256(sizeof(float) * size_t(q_grid_n(p, R, G)) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
+  float* gring = R + G > kRingMax && p.det ? (float*)w : nullptr;  // R = 128 determinant only
 
   // delta
   {
@@ -2054,6 +2165,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.dk2 = dk2;
     a.dv2 = dv2;
     a.band = band;
+    a.gring = gring;
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
     a.lR = __builtin_ctz(unsigned(R));
@@ -2068,18 +2180,23 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     };
     // staged rows: q, dO (G each) + k2, v2 (R+G-1 each) double-buffered; the ring holds R+G rows
     const bool staged = G <= 16 && 2 * G + 2 * (R + G - 1) <= kQStageRows && R + G <= 36;
+    const bool gr = R + G > kRingMax;  // R = 128: the ring lives in the global slab
 #define SA_Q_LAUNCH(DD, DET, RING, STG) launch(tc_bwd_q_kernel<DD, DET, RING, STG>, sizeof(QSmem<DD, RING, STG>) + 1024)
+#define SA_Q_PICK(DD, DET)                                                                             \
+  (gr ? SA_Q_LAUNCH(DD, DET, DET ? 129 : 130, false)                                                  \
+      : staged ? SA_Q_LAUNCH(DD, DET, 36, true) : SA_Q_LAUNCH(DD, DET, 66, false))
     if (p.D == 128) {
       if (p.det)
-        staged ? SA_Q_LAUNCH(128, true, 36, true) : SA_Q_LAUNCH(128, true, 66, false);
+        SA_Q_PICK(128, true);
       else
-        staged ? SA_Q_LAUNCH(128, false, 36, true) : SA_Q_LAUNCH(128, false, 66, false);
+        SA_Q_PICK(128, false);
     } else {
       if (p.det)
-        staged ? SA_Q_LAUNCH(64, true, 36, true) : SA_Q_LAUNCH(64, true, 66, false);
+        SA_Q_PICK(64, true);
       else
-        staged ? SA_Q_LAUNCH(64, false, 36, true) : SA_Q_LAUNCH(64, false, 66, false);
+        SA_Q_PICK(64, false);
     }
+#undef SA_Q_PICK
 #undef SA_Q_LAUNCH
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -85,6 +85,9 @@ def test_fp32_shapes(B, N, H, D, w1, w2, det):
     (1, 200, 2, 128, 32, 8),     # R = 8 (G = 16): the memory-bound small-window point of §8(d)
     (1, 96, 1, 64, 20, 4),       # R = 4
     (1, 70, 1, 128, 10, 2),      # R = 2 (G = 64)
+    (1, 400, 1, 128, 128, 128),  # R = 128 (G = 1): Table 1's (128, 128) row, dK'/dV' ring in global memory
+    (1, 300, 2, 64, 200, 128),   # R = 128, D = 64, ragged
+    (1, 260, 1, 128, 128, 300),  # w2 > w1 = 128: swapped, R = 128
 ])
 def test_bf16_shapes(B, N, H, D, w1, w2, det, force_simt):
     inp = make_inputs(B, N, H, D, seed=7 * N + D, dtype="bf16")
@@ -313,3 +316,10 @@ def test_bias(dtype, tol, H, Hk, D, w1, w2, det):
         assert torch.equal(oa, o_d)
         for lf, gd in zip(leaves, g_d):
             assert torch.equal(lf.grad, gd)
+
+
+@pytest.mark.parametrize("det", [False, True])
+def test_r128_backward_on_tcgen05(det):
+    """w2 = 128 (Table 1's (128, 128) row) runs the tcgen05 backward, not the CUDA-core path."""
+    assert sa.bwd_path(1, 16, 8192, 128, 128, 128, det=det) == sa.SA_PATH_TCGEN05
+    assert sa.fwd_path(1, 16, 8192, 128, 128, 128, det=det) == sa.SA_PATH_TCGEN05
