@@ -582,26 +582,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-      } else if (a.R == 64) {
-        // one query == two warps (lane quarters qd, qd^1): warp-level statistics by shuffles, the
-        // partner's partials through shared memory; each warp reduce-scatters its 32 rows, the even
-        // warp adds the odd warp's column partials and writes o
+      } else if (a.R == 64 || a.R == 128) {
+        // one query == two warps (R = 64: lane quarters qd, qd^1) or all four (R = 128): warp-level
+        // statistics by shuffles, the other warps' partials through shared memory; each warp
+        // reduce-scatters its 32 rows, the query's lead warp adds the others' column partials
+        const bool r128 = a.R == 128;
         const bool live = valid && m_ref != -INFINITY;
         float M = live ? m_ref : -INFINITY;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         if (lane == 0) sm.gM[x][qd] = M;
         named_bar_sync(1 + x, 128);
-        M = fmaxf(M, sm.gM[x][qd ^ 1]);
+        M = r128 ? fmaxf(fmaxf(sm.gM[x][0], sm.gM[x][1]), fmaxf(sm.gM[x][2], sm.gM[x][3]))
+                 : fmaxf(M, sm.gM[x][qd ^ 1]);
         const float crow = live ? ex2(m_ref - M) : 0.f;
         float L = live ? l * crow : 0.f;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
         if (lane == 0) sm.gL[x][qd] = L;
         named_bar_sync(1 + x, 128);
-        L += sm.gL[x][qd ^ 1];
+        L = r128 ? (sm.gL[x][0] + sm.gL[x][1]) + (sm.gL[x][2] + sm.gL[x][3]) : L + sm.gL[x][qd ^ 1];
         const bool qlive = g < nq;
-        const bool lead = (qd & 1) == 0;
+        const bool lead = r128 ? qd == 0 : (qd & 1) == 0;
         if (lead && lane == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
         const float invL = qlive ? 1.f / L : 0.f;
 #pragma unroll 1
@@ -648,7 +650,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!lead && (lane & 1) == 0) part[col] = v[0];
           named_bar_sync(1 + x, 128);
           if (lead && (lane & 1) == 0 && qlive) {
-            const float y = v[0] + sm.ebuf[x][(cb & 1) * 4 + (qd ^ 1)][col];
+            const float* eb4 = &sm.ebuf[x][(cb & 1) * 4][col];  // rows qd' = 0..3, pitch 17
+            const float y = r128 ? v[0] + (eb4[17] + eb4[2 * 17]) + eb4[3 * 17] : v[0] + eb4[(qd ^ 1) * 17];
             const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + col;
             if (a.out_f32)
               reinterpret_cast<float*>(a.o)[off] = y * invL;
