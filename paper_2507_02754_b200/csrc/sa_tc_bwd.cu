@@ -92,7 +92,7 @@ struct QSmem {
   static constexpr int kStages = kG1 ? 2 : 3;
   static constexpr int kPanelBytes = kQChunk * 128;
   static constexpr int kStageBytes = kQChunk * D * 2;
-  static constexpr int kAP = kG1 ? D + 4 : D;  // ring pitch (floats)
+  static constexpr int kAP = kGR ? D : D + 4;  // ring pitch (floats): padded for row-owned float4 updates
   static constexpr int kEB = kG1 ? 1 : 128;    // eb rows (unused by the G = 1 pass)
   alignas(1024) uint8_t k[kStages][kStageBytes];
   alignas(1024) uint8_t v[kStages][kStageBytes];
@@ -110,7 +110,7 @@ struct QSmem {
   alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D + 8];
   float slse[2][16], sdl[2][16];
   float dqx[2][32];  // R = 64: the odd lane quarter's dq column partials of the current pass
-  float dq4[kG1 ? 4 : 1][D];  // R = 128 trilinear: per-lane-quarter dq partials
+  float dq4[4][D];  // R = 64 / 128 trilinear: per-lane-quarter dq partials
   uint64_t kvfull[kStages], kvempty[kStages];
   uint64_t sfull[2], pready[2], udone, aready;
   uint32_t tmem_base;
@@ -503,6 +503,92 @@ __device__ __forceinline__ void q_epilogue_g1(QSmem<D, RING, STAGED>& sm, const 
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
   const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
   if ((ln & 3) == 0) sm.dq4[r >> 5][cs + col] = v[0];
+}
+
+// R = 32 / 64 trilinear, row-owned: phase ph (0..3) of lane quarter qd (query g = qd >> (lR - 5))
+// covers column block (ph + g * 4/G) & 3 (32 columns; warp m = 2 half + sub takes 8 of them).  The
+// rows that share a key row belong to different queries, hence different column blocks in every
+// phase, so each thread adds its row's s q o W and dO o U straight into the ring (padded pitch) with
+// no gather; one barrier per phase separates the blocks.  dq: register reduce-scatter over the
+// warp's 32 rows; R = 32 writes it, R = 64 parks the quarter's partial in dq4 (summed by the caller).
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                               int ph, int half, int sub, int r, bool valid, const QRows& rw,
+                                               uint32_t tW, uint32_t tU, int sbase) {
+  const Problem& p = a.p;
+  const float s = p.scale;
+  const int ln = r & 31, qd = r >> 5;
+  const int g = r >> a.lR;
+  const int m = 2 * half + sub;
+  const int blk = (ph + g * (4 / a.G)) & 3;
+  const int cs = 32 * blk + 8 * m;
+  uint32_t uw[8], uu[8];
+  tmem_ld8(tW + cs, uw);
+  tmem_ld8(tU + cs, uu);
+  float k2v[8], qv[8], dov[8];
+  if (valid) {
+    load_f16<8>(rw.k2 + cs, k2v);
+    load_f16<8>(rw.q + cs, qv);
+    load_f16<8>(rw.dO + cs, dov);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
+  }
+  int slot = sbase + (r & (a.R - 1)) + g;  // key row P0 - R + 1 + g + kk
+  if (slot >= a.ring) slot -= a.ring;
+  auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
+  float4 xk0 = make_float4(0.f, 0.f, 0.f, 0.f), xk1 = xk0, xv0 = xk0, xv1 = xk0;
+  if (valid) {
+    xk0 = *reinterpret_cast<const float4*>(&ak[slot][cs]);
+    xk1 = *reinterpret_cast<const float4*>(&ak[slot][cs + 4]);
+    xv0 = *reinterpret_cast<const float4*>(&av[slot][cs]);
+    xv1 = *reinterpret_cast<const float4*>(&av[slot][cs + 4]);
+  }
+  tmem_ld_wait();
+  float v[8], ck[8], cv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float w = __uint_as_float(uw[e]);
+    v[e] = s * k2v[e] * w;
+    ck[e] = s * qv[e] * w;
+    cv[e] = dov[e] * __uint_as_float(uu[e]);
+  }
+  if (valid) {
+    *reinterpret_cast<float4*>(&ak[slot][cs]) =
+        make_float4(xk0.x + ck[0], xk0.y + ck[1], xk0.z + ck[2], xk0.w + ck[3]);
+    *reinterpret_cast<float4*>(&ak[slot][cs + 4]) =
+        make_float4(xk1.x + ck[4], xk1.y + ck[5], xk1.z + ck[6], xk1.w + ck[7]);
+    *reinterpret_cast<float4*>(&av[slot][cs]) =
+        make_float4(xv0.x + cv[0], xv0.y + cv[1], xv0.z + cv[2], xv0.w + cv[3]);
+    *reinterpret_cast<float4*>(&av[slot][cs + 4]) =
+        make_float4(xv1.x + cv[4], xv1.y + cv[5], xv1.z + cv[6], xv1.w + cv[7]);
+  }
+#pragma unroll
+  for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+    const bool hi = ln & st;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+    }
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+  if ((ln & 3) == 0) {
+    if (a.R == 32) {
+      if (g < it.nq) {
+        const int64_t off = p.qoff(it.b, it.i0 + g, it.h) + cs + col;
+        if (a.out_f32)
+          reinterpret_cast<float*>(a.dq)[off] = v[0];
+        else
+          reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+      }
+    } else {
+      sm.dq4[qd][cs + col] = v[0];
+    }
+  }
+  named_bar_sync(1, kQNT);
 }
 
 // Determinant pass over 24 columns [c0, c0+24) (eight 3-chunks), R in {32, 64}: warp m = 2 half + sub
@@ -1254,6 +1340,24 @@ __global__ void __launch_bounds__(kQThreads, 1)
         if constexpr (D % 24 != 0)
           q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256,
                                                         sub == 0);
+      } else if (D == 128 && (a.R == 32 || a.R == 64)) {
+        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+#pragma unroll 1
+        for (int ph = 0; ph < 4; ++ph) {
+          q_epilogue_rot<D, RING, STAGED>(sm, a, it, ph, half, sub, r, valid, rw, tW, tU, sbase);
+          SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | ph);
+        }
+        if (a.R == 64 && tid256 < 2 * D) {  // dq = the two lane quarters' partials of each query
+          const int gq = tid256 / D, d = tid256 % D;
+          if (gq < it.nq) {
+            const float y = sm.dq4[2 * gq][d] + sm.dq4[2 * gq + 1][d];
+            const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + d;
+            if (a.out_f32)
+              reinterpret_cast<float*>(a.dq)[off] = y;
+            else
+              reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
+          }
+        }
       } else if (a.R == 32 || a.R == 64) {
 #pragma unroll 1
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
