@@ -513,82 +513,105 @@ __device__ __forceinline__ void q_epilogue_g1(QSmem<D, RING, STAGED>& sm, const 
 // warp's 32 rows; R = 32 writes it, R = 64 parks the quarter's partial in dq4 (summed by the caller).
 template <int D, int RING, bool STAGED>
 __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
-                                               int ph, int half, int sub, int r, bool valid, const QRows& rw,
+                                               int half, int sub, int r, bool valid, const QRows& rw,
                                                uint32_t tW, uint32_t tU, int sbase) {
   const Problem& p = a.p;
   const float s = p.scale;
   const int ln = r & 31, qd = r >> 5;
   const int g = r >> a.lR;
   const int m = 2 * half + sub;
-  const int blk = (ph + g * (4 / a.G)) & 3;
-  const int cs = 32 * blk + 8 * m;
-  uint32_t uw[8], uu[8];
-  tmem_ld8(tW + cs, uw);
-  tmem_ld8(tU + cs, uu);
-  float k2v[8], qv[8], dov[8];
-  if (valid) {
-    load_f16<8>(rw.k2 + cs, k2v);
-    load_f16<8>(rw.q + cs, qv);
-    load_f16<8>(rw.dO + cs, dov);
-  } else {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
-  }
+  const int rot = g * (4 / a.G);
   int slot = sbase + (r & (a.R - 1)) + g;  // key row P0 - R + 1 + g + kk
   if (slot >= a.ring) slot -= a.ring;
   auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
-  float4 xk0 = make_float4(0.f, 0.f, 0.f, 0.f), xk1 = xk0, xv0 = xk0, xv1 = xk0;
+  // operands of phase ph+1 (TMEM W/U columns, fp16 row chunks) are requested before phase ph's
+  // reduction and barrier, so their latency overlaps them
+  uint32_t uw[8], uu[8];
+  uint4 rk2 = make_uint4(0u, 0u, 0u, 0u), rq = rk2, rdo = rk2;
+  int cs = 32 * (rot & 3) + 8 * m;
+  tmem_ld8(tW + cs, uw);
+  tmem_ld8(tU + cs, uu);
   if (valid) {
-    xk0 = *reinterpret_cast<const float4*>(&ak[slot][cs]);
-    xk1 = *reinterpret_cast<const float4*>(&ak[slot][cs + 4]);
-    xv0 = *reinterpret_cast<const float4*>(&av[slot][cs]);
-    xv1 = *reinterpret_cast<const float4*>(&av[slot][cs + 4]);
-  }
-  tmem_ld_wait();
-  float v[8], ck[8], cv[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const float w = __uint_as_float(uw[e]);
-    v[e] = s * k2v[e] * w;
-    ck[e] = s * qv[e] * w;
-    cv[e] = dov[e] * __uint_as_float(uu[e]);
-  }
-  if (valid) {
-    *reinterpret_cast<float4*>(&ak[slot][cs]) =
-        make_float4(xk0.x + ck[0], xk0.y + ck[1], xk0.z + ck[2], xk0.w + ck[3]);
-    *reinterpret_cast<float4*>(&ak[slot][cs + 4]) =
-        make_float4(xk1.x + ck[4], xk1.y + ck[5], xk1.z + ck[6], xk1.w + ck[7]);
-    *reinterpret_cast<float4*>(&av[slot][cs]) =
-        make_float4(xv0.x + cv[0], xv0.y + cv[1], xv0.z + cv[2], xv0.w + cv[3]);
-    *reinterpret_cast<float4*>(&av[slot][cs + 4]) =
-        make_float4(xv1.x + cv[4], xv1.y + cv[5], xv1.z + cv[6], xv1.w + cv[7]);
+    rk2 = *reinterpret_cast<const uint4*>(rw.k2 + cs);
+    rq = *reinterpret_cast<const uint4*>(rw.q + cs);
+    rdo = *reinterpret_cast<const uint4*>(rw.dO + cs);
   }
 #pragma unroll
-  for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
-    const bool hi = ln & st;
-#pragma unroll
-    for (int i = 0; i < n; ++i) {
-      const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+  for (int ph = 0; ph < 4; ++ph) {
+    float4 xk0 = make_float4(0.f, 0.f, 0.f, 0.f), xk1 = xk0, xv0 = xk0, xv1 = xk0;
+    if (valid) {
+      xk0 = *reinterpret_cast<const float4*>(&ak[slot][cs]);
+      xk1 = *reinterpret_cast<const float4*>(&ak[slot][cs + 4]);
+      xv0 = *reinterpret_cast<const float4*>(&av[slot][cs]);
+      xv1 = *reinterpret_cast<const float4*>(&av[slot][cs + 4]);
     }
-  }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
-  if ((ln & 3) == 0) {
-    if (a.R == 32) {
-      if (g < it.nq) {
-        const int64_t off = p.qoff(it.b, it.i0 + g, it.h) + cs + col;
-        if (a.out_f32)
-          reinterpret_cast<float*>(a.dq)[off] = v[0];
-        else
-          reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+    tmem_ld_wait();
+    float v[8], ck[8], cv[8];
+    {
+      const uint32_t ks[4] = {rk2.x, rk2.y, rk2.z, rk2.w}, qs[4] = {rq.x, rq.y, rq.z, rq.w},
+                     ds[4] = {rdo.x, rdo.y, rdo.z, rdo.w};
+#pragma unroll
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float2 kf = __half22float2(*reinterpret_cast<const __half2*>(&ks[e2]));
+        const float2 qf = __half22float2(*reinterpret_cast<const __half2*>(&qs[e2]));
+        const float2 df = __half22float2(*reinterpret_cast<const __half2*>(&ds[e2]));
+        const float w0 = __uint_as_float(uw[2 * e2]), w1 = __uint_as_float(uw[2 * e2 + 1]);
+        v[2 * e2] = s * kf.x * w0;
+        v[2 * e2 + 1] = s * kf.y * w1;
+        ck[2 * e2] = s * qf.x * w0;
+        ck[2 * e2 + 1] = s * qf.y * w1;
+        cv[2 * e2] = df.x * __uint_as_float(uu[2 * e2]);
+        cv[2 * e2 + 1] = df.y * __uint_as_float(uu[2 * e2 + 1]);
       }
-    } else {
-      sm.dq4[qd][cs + col] = v[0];
     }
+    if (valid) {
+      *reinterpret_cast<float4*>(&ak[slot][cs]) =
+          make_float4(xk0.x + ck[0], xk0.y + ck[1], xk0.z + ck[2], xk0.w + ck[3]);
+      *reinterpret_cast<float4*>(&ak[slot][cs + 4]) =
+          make_float4(xk1.x + ck[4], xk1.y + ck[5], xk1.z + ck[6], xk1.w + ck[7]);
+      *reinterpret_cast<float4*>(&av[slot][cs]) =
+          make_float4(xv0.x + cv[0], xv0.y + cv[1], xv0.z + cv[2], xv0.w + cv[3]);
+      *reinterpret_cast<float4*>(&av[slot][cs + 4]) =
+          make_float4(xv1.x + cv[4], xv1.y + cv[5], xv1.z + cv[6], xv1.w + cv[7]);
+    }
+    const int csd = cs;
+    if (ph < 3) {
+      cs = 32 * ((ph + 1 + rot) & 3) + 8 * m;
+      tmem_ld8(tW + cs, uw);
+      tmem_ld8(tU + cs, uu);
+      if (valid) {
+        rk2 = *reinterpret_cast<const uint4*>(rw.k2 + cs);
+        rq = *reinterpret_cast<const uint4*>(rw.q + cs);
+        rdo = *reinterpret_cast<const uint4*>(rw.dO + cs);
+      }
+    }
+#pragma unroll
+    for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+      const bool hi = ln & st;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+      }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+    if ((ln & 3) == 0) {
+      if (a.R == 32) {
+        if (g < it.nq) {
+          const int64_t off = p.qoff(it.b, it.i0 + g, it.h) + csd + col;
+          if (a.out_f32)
+            reinterpret_cast<float*>(a.dq)[off] = v[0];
+          else
+            reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+        }
+      } else {
+        sm.dq4[qd][csd + col] = v[0];
+      }
+    }
+    named_bar_sync(1, kQNT);
   }
-  named_bar_sync(1, kQNT);
 }
 
 // Determinant pass over 24 columns [c0, c0+24) (eight 3-chunks), R in {32, 64}: warp m = 2 half + sub
@@ -1342,11 +1365,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
                                                         sub == 0);
       } else if (D == 128 && (a.R == 32 || a.R == 64)) {
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
-#pragma unroll 1
-        for (int ph = 0; ph < 4; ++ph) {
-          q_epilogue_rot<D, RING, STAGED>(sm, a, it, ph, half, sub, r, valid, rw, tW, tU, sbase);
-          SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | ph);
-        }
+        q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
         if (a.R == 64 && tid256 < 2 * D) {  // dq = the two lane quarters' partials of each query
           const int gq = tid256 / D, d = tid256 % D;
           if (gq < it.nq) {
