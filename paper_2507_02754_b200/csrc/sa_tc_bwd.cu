@@ -87,13 +87,15 @@ struct QSmem {
   // RING variants: <= kRingMax shared-memory ring (R <= 64); 129: R = 128 determinant, ring in the
   // global slab BwdQArgs::gring (generic passes); 130: R = 128 trilinear (G = 1), ring in shared
   // memory with a padded pitch (row-owned updates, q_epilogue_g1), two K/V stages to make room
+  // 37 / 67: R = 32 / 64 trilinear at D = 128 (row-owned q_epilogue_rot, no eb): four K/V stages
   static constexpr bool kGR = RING == 129;
   static constexpr bool kG1 = RING == 130;
-  static constexpr int kStages = kG1 ? 2 : 3;
+  static constexpr bool kRot = RING == 37 || RING == 67;
+  static constexpr int kStages = kG1 ? 2 : kRot ? 4 : 3;
   static constexpr int kPanelBytes = kQChunk * 128;
   static constexpr int kStageBytes = kQChunk * D * 2;
   static constexpr int kAP = kGR ? D : D + 4;  // ring pitch (floats): padded for row-owned float4 updates
-  static constexpr int kEB = kG1 ? 1 : 128;    // eb rows (unused by the G = 1 pass)
+  static constexpr int kEB = (kG1 || kRot) ? 1 : 128;  // eb rows (unused by the row-owned passes)
   alignas(1024) uint8_t k[kStages][kStageBytes];
   alignas(1024) uint8_t v[kStages][kStageBytes];
   alignas(16) float acc_k2[kGR ? 1 : RING][kAP];
@@ -1351,19 +1353,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           else
             reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
         }
-      } else if (DET && (a.R == 32 || a.R == 64)) {
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
-#pragma unroll 1
-        for (int c0 = 0; c0 < D; c0 += 24)
-          q_epilogue_pass_det<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
-      } else if (DET) {
-#pragma unroll 1
-        for (int c0 = 0; c0 + 24 <= D; c0 += 24)
-          q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256, sub == 0);
-        if constexpr (D % 24 != 0)
-          q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256,
-                                                        sub == 0);
-      } else if (D == 128 && (a.R == 32 || a.R == 64)) {
+      } else if constexpr (Sm::kRot) {
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
         q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
         if (a.R == 64 && tid256 < 2 * D) {  // dq = the two lane quarters' partials of each query
@@ -1377,6 +1367,18 @@ __global__ void __launch_bounds__(kQThreads, 1)
               reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
           }
         }
+      } else if (DET && (a.R == 32 || a.R == 64)) {
+        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 24)
+          q_epilogue_pass_det<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
+      } else if (DET) {
+#pragma unroll 1
+        for (int c0 = 0; c0 + 24 <= D; c0 += 24)
+          q_epilogue_pass<D, RING, STAGED, 24, DET>(sm, a, it, c0, half, r, valid, rw, tW, tU, tid256, sub == 0);
+        if constexpr (D % 24 != 0)
+          q_epilogue_pass<D, RING, STAGED, D % 24, DET>(sm, a, it, D - D % 24, half, r, valid, rw, tW, tU, tid256,
+                                                        sub == 0);
       } else if (a.R == 32 || a.R == 64) {
 #pragma unroll 1
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
@@ -2305,8 +2307,10 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     const bool staged = G <= 16 && 2 * G + 2 * (R + G - 1) <= kQStageRows && R + G <= 36;
     const bool gr = R + G > kRingMax;  // R = 128: the ring lives in the global slab
 #define SA_Q_LAUNCH(DD, DET, RING, STG) launch(tc_bwd_q_kernel<DD, DET, RING, STG>, sizeof(QSmem<DD, RING, STG>) + 1024)
+    const bool rot = !p.det && p.D == 128 && (R == 32 || R == 64);  // row-owned epilogue, 4 K/V stages
 #define SA_Q_PICK(DD, DET)                                                                             \
   (gr ? SA_Q_LAUNCH(DD, DET, DET ? 129 : 130, false)                                                  \
+      : (!DET && DD == 128 && rot) ? (staged ? SA_Q_LAUNCH(DD, DET, 37, true) : SA_Q_LAUNCH(DD, DET, 67, false)) \
       : staged ? SA_Q_LAUNCH(DD, DET, 36, true) : SA_Q_LAUNCH(DD, DET, 66, false))
     if (p.D == 128) {
       if (p.det)
