@@ -604,37 +604,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool lead = r128 ? qd == 0 : (qd & 1) == 0;
         if (lead && lane == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
         const float invL = qlive ? 1.f / L : 0.f;
-#pragma unroll 1
-        for (int cb = 0; cb < D / 16; ++cb) {
-          uint32_t u[16];
-          tmem_ld16(tU + 16 * cb, u);
+        // 32-column blocks as in the R = 32 path (column `lane` in lane `lane` after the reduce-
+        // scatter); the other warps' column partials go through ebuf (flat, 32 per warp, double-
+        // buffered by block parity), one barrier per block
+        float* ebf = &sm.ebuf[x][0][0];
+        uint32_t u[32];
+        uint4 y[4] = {};
+        tmem_ld32(tU, u);
+        if (valid) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) y[t] = *reinterpret_cast<const uint4*>(v2row + 8 * t);
+        }
+#pragma unroll
+        for (int cb = 0; cb < D / 32; ++cb) {
           tmem_ld_wait();
-          float v[16];
-          if (valid) {
-            if (STAGED) {
-              const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
+          float v[32];
 #pragma unroll
-              for (int t = 0; t < 2; ++t) {
-                const uint4 y = vp[t];
-                const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t ys[4] = {y[t].x, y[t].y, y[t].z, y[t].w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = bf16x2_to_f2(ys[e]);
-                  v[8 * t + 2 * e] = f.x;
-                  v[8 * t + 2 * e + 1] = f.y;
-                }
-              }
-            } else {
-              load_bf16<16>(v2row + 16 * cb, v);
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = bf16x2_to_f2(ys[e]);
+              v[8 * t + 2 * e] = f.x * crow * __uint_as_float(u[8 * t + 2 * e]);
+              v[8 * t + 2 * e + 1] = f.y * crow * __uint_as_float(u[8 * t + 2 * e + 1]);
             }
+          }
+          if (cb + 1 < D / 32) {
+            tmem_ld32(tU + 32 * (cb + 1), u);
+            if (valid) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] *= crow * __uint_as_float(u[e]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = 0.f;
+              for (int t = 0; t < 4; ++t) y[t] = *reinterpret_cast<const uint4*>(v2row + 32 * (cb + 1) + 8 * t);
+            }
           }
 #pragma unroll
-          for (int st = 16, n = 8; st >= 2; st >>= 1, n >>= 1) {
+          for (int st = 16, n = 16; st >= 1; st >>= 1, n >>= 1) {
             const bool hi = lane & st;
 #pragma unroll
             for (int i = 0; i < n; ++i) {
@@ -642,19 +645,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
             }
           }
-          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-          const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-          float* part = &sm.ebuf[x][(cb & 1) * 4 + qd][0];  // column partials, double-buffered by cb parity
-          if (!lead && (lane & 1) == 0) part[col] = v[0];
+          float* part = ebf + ((cb & 1) * 4) * 32;
+          if (!lead) part[qd * 32 + lane] = v[0];
           named_bar_sync(1 + x, 128);
-          if (lead && (lane & 1) == 0 && qlive) {
-            const float* eb4 = &sm.ebuf[x][(cb & 1) * 4][col];  // rows qd' = 0..3, pitch 17
-            const float y = r128 ? v[0] + (eb4[17] + eb4[2 * 17]) + eb4[3 * 17] : v[0] + eb4[(qd ^ 1) * 17];
-            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + col;
+          if (lead && qlive) {
+            const float yv = r128 ? v[0] + (part[32 + lane] + part[64 + lane]) + part[96 + lane]
+                                  : v[0] + part[(qd ^ 1) * 32 + lane];
+            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 32 * cb + lane;
             if (a.out_f32)
-              reinterpret_cast<float*>(a.o)[off] = y * invL;
+              reinterpret_cast<float*>(a.o)[off] = yv * invL;
             else
-              reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(y * invL);
+              reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(yv * invL);
           }
         }
       } else {
