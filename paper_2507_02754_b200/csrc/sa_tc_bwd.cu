@@ -109,7 +109,15 @@ struct QSmem {
     } w;  // R = 32 trilinear passes (PW = 32, dq reduced in registers)
   } eb;
   // staged rows; pitch D+8 halves so that lanes reading consecutive rows hit distinct banks
-  alignas(16) __half stg[STAGED ? 2 : 1][STAGED ? kQStageRows : 1][D + 8];
+  // kRing (kRot and STAGED, R = 32): q/dO rows double-buffered per item; k2/v2 rows in a ring keyed
+  // by key position (slot kpos % kKR), one ring half per (b,h) run of the CTA's contiguous items, so
+  // consecutive items stage only their G new key rows
+  static constexpr bool kRing = kRot && STAGED;
+  static constexpr int kKR = 40;  // ring slots per half (>= R + 2G - 1 = 39)
+  alignas(16) __half stg[(STAGED && !kRing) ? 2 : 1][(STAGED && !kRing) ? kQStageRows : 1][D + 8];
+  alignas(16) __half stgq[kRing ? 2 : 1][kRing ? 8 : 1][D + 8];  // q rows 0..G-1, dO rows G..2G-1
+  alignas(16) __half rk2[kRing ? 2 : 1][kRing ? kKR : 1][D + 8];
+  alignas(16) __half rv2[kRing ? 2 : 1][kRing ? kKR : 1][D + 8];
   float slse[2][16], sdl[2][16];
   float dqx[2][32];  // R = 64: the odd lane quarter's dq column partials of the current pass
   float dq4[4][D];  // R = 64 / 128 trilinear: per-lane-quarter dq partials
@@ -1079,6 +1087,42 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         return;
       }
+      if constexpr (Sm::kRing) {
+        const QItem it = q_item(a, item);
+        const int P0 = p.np + it.i0;
+        const bool fresh = item == it_begin || it.grp == 0;  // first item of a (b,h) run: whole window
+        const int rh = (it.bh - it_begin / a.ngroups) & 1;
+        const int klo = fresh ? P0 - a.R + 1 : P0;
+        const int nkn = P0 + a.G - klo;  // key rows to stage
+        const int nrows = 2 * a.G + 2 * nkn;
+        for (int task = tid256; task < nrows * kC8; task += kQNT) {
+          const int row = task / kC8, c8 = task % kC8;
+          const __half* src = nullptr;
+          __half* dst;
+          if (row < 2 * a.G) {
+            const int gq = row < a.G ? row : row - a.G;
+            if (gq < it.nq) src = (row < a.G ? a.q : a.dO) + p.qoff(it.b, it.i0 + gq, it.h);
+            dst = &sm.stgq[buf][row][0];
+          } else {
+            const int rr = row - 2 * a.G;
+            const bool isv = rr >= nkn;
+            const int kp = klo + (isv ? rr - nkn : rr);
+            if (kp >= 0 && kp < p.NK()) src = (isv ? a.v2 : a.k2) + p.kvoff(it.b, kp, it.hk);
+            dst = isv ? &sm.rv2[rh][kp >= 0 ? kp % Sm::kKR : 0][0] : &sm.rk2[rh][kp >= 0 ? kp % Sm::kKR : 0][0];
+          }
+          if (src) cp_async16(dst + 8 * c8, src + 8 * c8);
+        }
+        if (tid256 < 2 * it.nq) {
+          const int g = tid256 < it.nq ? tid256 : tid256 - it.nq;
+          const int64_t x = (int64_t(it.b) * p.H + it.h) * p.N + it.i0 + g;
+          if (tid256 < it.nq)
+            cp_async4(&sm.slse[buf][g], a.lse + x);
+          else
+            cp_async4(&sm.sdl[buf][g], a.delta + x);
+        }
+        cp_async_commit();
+        return;
+      }
       const QItem it = q_item(a, item);
       const int P0 = p.np + it.i0;
       const int nk = a.R + a.G - 1;
@@ -1123,7 +1167,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
       QRows fr{};
       if (fvalid) {
         const int nk = a.R + a.G - 1;
-        if (STAGED) {
+        if constexpr (Sm::kRing) {
+          const int rh = (fi.bh - it_begin / a.ngroups) & 1;
+          fr.q = &sm.stgq[bf][g][0];
+          fr.dO = &sm.stgq[bf][a.G + g][0];
+          fr.k2 = &sm.rk2[rh][fkpos % Sm::kKR][0];
+          fr.v2 = &sm.rv2[rh][fkpos % Sm::kKR][0];
+        } else if (STAGED) {
           fr.q = &sm.stg[bf][g][0];
           fr.dO = &sm.stg[bf][a.G + g][0];
           fr.k2 = &sm.stg[bf][2 * a.G + g + kk][0];
@@ -1263,7 +1313,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
       }
       if (valid) {
         const int nk = a.R + a.G - 1;
-        if (STAGED) {
+        if constexpr (Sm::kRing) {
+          const int rh = (it.bh - it_begin / a.ngroups) & 1;
+          rw.q = &sm.stgq[buf][g][0];
+          rw.dO = &sm.stgq[buf][a.G + g][0];
+          rw.k2 = &sm.rk2[rh][kpos % Sm::kKR][0];
+          rw.v2 = &sm.rv2[rh][kpos % Sm::kKR][0];
+        } else if (STAGED) {
           rw.q = &sm.stg[buf][g][0];
           rw.dO = &sm.stg[buf][a.G + g][0];
           rw.k2 = &sm.stg[buf][2 * a.G + g + kk][0];
