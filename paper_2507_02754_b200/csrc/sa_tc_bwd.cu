@@ -524,7 +524,8 @@ __device__ __forceinline__ void q_epilogue_g1(QSmem<D, RING, STAGED>& sm, const 
 template <int D, int RING, bool STAGED>
 __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
                                                int half, int sub, int r, bool valid, const QRows& rw,
-                                               uint32_t tW, uint32_t tU, int sbase) {
+                                               uint32_t tW, uint32_t tU, int sbase, bool tr, int treg, int& trn,
+                                               int titem) {
   const Problem& p = a.p;
   const float s = p.scale;
   const int ln = r & 31, qd = r >> 5;
@@ -585,6 +586,7 @@ __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const
           make_float4(xv1.x + cv[4], xv1.y + cv[5], xv1.z + cv[6], xv1.w + cv[7]);
     }
     const int csd = cs;
+    SA_TRACE_AT(tr, treg, trn, titem << 16 | 12 << 8 | ph);
     if (ph < 3) {
       cs = 32 * ((ph + 1 + rot) & 3) + 8 * m;
       tmem_ld8(tW + cs, uw);
@@ -621,6 +623,7 @@ __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const
       }
     }
     named_bar_sync(1, kQNT);
+    SA_TRACE_AT(tr, treg, trn, titem << 16 | 13 << 8 | ph);
   }
 }
 
@@ -1411,7 +1414,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
       } else if constexpr (Sm::kRot) {
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
-        q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
+        q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase, tr, treg, trn,
+                                        item - it_begin);
         if (a.R == 64 && tid256 < 2 * D) {  // dq = the two lane quarters' partials of each query
           const int gq = tid256 / D, d = tid256 % D;
           if (gq < it.nq) {
@@ -1492,6 +1496,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
       }
       flush_lo = flush_hi + 1;
+      SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 14 << 8);
       named_bar_sync(1, kQNT);
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 7 << 8);
       kc += it.nch;
