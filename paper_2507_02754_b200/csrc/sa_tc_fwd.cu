@@ -421,12 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 pv = (t & 7) == 7 ? ex2_poly2(xx) : make_float2(ex2(xx.x), ex2(xx.y));
           ls4[t & 3] = fadd2(ls4[t & 3], pv);  // 4 independent packed partial sums
           pk[t] = pack_f16x2(pv);
+          if (t == 15 && w >= 32) tmem_st16(tS, pk);  // first 32 columns go out while the rest compute
         }
         const float ls = ((ls4[0].x + ls4[0].y) + (ls4[1].x + ls4[1].y)) + ((ls4[2].x + ls4[2].y) + (ls4[3].x + ls4[3].y));
         l += ls;  // columns >= w were masked to -inf above (need_mask holds whenever w < 64)
         SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 24 << 8 | c);
-        if (w == 64) tmem_st32(tS, pk);
-        if (w == 32 || w == 48) tmem_st16(tS, pk);
+        if (w == 64) tmem_st16(tS + 16, pk + 16);
         if (w == 48) tmem_st8(tS + 16, pk + 16);
         if (w == 16) tmem_st8(tS, pk);
         tmem_st_wait();
