@@ -321,11 +321,13 @@ def run_membound(args, c):
     }), flush=True)
 
 
-def config_block(c, n, mode="bh"):
+def config_block(c, n, mode="bh", scaling="weak"):
+    per = "per GPU" if scaling == "weak" else f"sharded over {n} GPU(s)"
     return {"workload": f"{c['name']}: B={c['B']} H={c['H']} N={c['N']} D={c['D']} w1={c['w1']} w2={c['w2']} "
-                        f"{'det' if c['det'] else 'trilinear'} {'fwd+bwd' if c['bwd'] else 'fwd'} per GPU",
+                        f"{'det' if c['det'] else 'trilinear'} {'fwd+bwd' if c['bwd'] else 'fwd'} {per}",
             "B": c["B"], "H": c["H"], "N": c["N"], "D": c["D"], "w1": c["w1"], "w2": c["w2"],
-            "variant": "det" if c["det"] else "trilinear", "global_batch_heads": c["B"] * c["H"] * n,
+            "variant": "det" if c["det"] else "trilinear",
+            "global_batch_heads": c["B"] * c["H"] * (n if scaling == "weak" else 1),
             "seq_len": c["N"], "parallelism": f"{mode}-sharded x{n}",
             "l2": "inputs larger than L2 (no flush): %.0f MB of inputs per step" % (
                 6 * c["B"] * c["N"] * c["H"] * c["D"] * 2 / 1e6),
@@ -347,8 +349,13 @@ def main():
                     help="table1: the paper's (w1, w2) latency sweep (Table 1, P:335-354) at the chosen "
                          "config's B, H, N, D; one JSON line per pair (not the bench line)")
     ap.add_argument("--mode", default="bh", choices=["bh", "seq"],
-                    help="bh: each rank runs its own B*H shard (weak scaling, no collective); seq: the "
-                         "sequence is split across ranks (N per rank fixed) with the NCCL halo exchange")
+                    help="bh: B*H sharding, no data-path collective; seq: the sequence is split across "
+                         "ranks with the NCCL halo exchange (parallel.seq_forward / seq_backward)")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="weak: every rank runs a whole config-sized problem of its own (c2-c4 default); "
+                         "strong: ONE config-sized problem (global seed) is sharded over the ranks -- "
+                         "parallel.bh_slice blocks in bh mode, N/world query rows in seq mode (c5 default, "
+                         "the long-context config BASELINE.json shards at 2/4/8 GPUs)")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config], name=args.config)
 
@@ -377,9 +384,33 @@ def main():
     sa.load_library(build=(rank == 0))
     if world > 1:
         dist.barrier()
+    scaling = args.scaling or ("strong" if args.config == "c5" else "weak")
+    if args.mode == "seq":
+        scaling = "strong" if args.scaling is None else scaling
     B, H, N, D, w1, w2, det = (c[k] for k in ("B", "H", "N", "D", "w1", "w2", "det"))
-    inp = make_inputs(B, N, H, D, seed_of(args.config, salt=rank), dtype=c["dtype"], device="cpu")
-    t = {n: x.to(dev) for n, x in inp.items()}
+    shard_desc = None
+    if scaling == "weak":
+        inp = make_inputs(B, N, H, D, seed_of(args.config, salt=rank), dtype=c["dtype"], device="cpu")
+        t = {n: x.to(dev) for n, x in inp.items()}
+    else:
+        # one global problem (global seed, drawn on the device -- the recipe's Generator(device)), each
+        # rank keeps its block: sharded and unsharded runs see identical data
+        from paper_2507_02754_b200 import parallel
+        full = make_inputs(B, N, H, D, seed_of(args.config), dtype=c["dtype"], device=str(dev))
+        if args.mode == "seq":
+            lo, hi, _ = parallel.seq_shard(N, rank, world, max(w1, w2) - 1)
+            t = {n: x[:, lo:hi].contiguous() for n, x in full.items()}
+            shard_desc = f"queries/keys [{lo}, {hi}) of N={N}"
+            N = hi - lo
+        else:
+            b0, b1, h0, h1 = parallel.bh_slice(B, H, rank, world)
+            t = {n: x[b0:b1, :, h0:h1].contiguous() for n, x in full.items()}
+            shard_desc = f"b [{b0}, {b1}) x h [{h0}, {h1}) of B={B} H={H}"
+            B, H = b1 - b0, h1 - h0
+        del full
+        torch.cuda.empty_cache()
+        inp = {n: x.cpu() for n, x in t.items()} if not args.no_e2e else None
+    cl = dict(c, B=B, H=H, N=N)  # this rank's problem
     out_bytes = 4 if args.out_f32 else 2
     ws = None
     o = lse = None
@@ -429,13 +460,15 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     which = ("fwd", "bwd") if c["bwd"] else ("fwd",)
-    flops_step = paper_flops(c, which) * world
+    # whole-job work per step: weak = every rank a whole config problem; strong = one problem
+    jobs = world if scaling == "weak" else 1
+    flops_step = paper_flops(c, which) * jobs
     value = flops_step * args.steps / (ms / 1e3) / 1e12
-    mma_flops_step = sum(MMA_FLOPS_PER_TRIPLE_D[w] for w in which) * nominal_triples(c) * D * world
+    mma_flops_step = sum(MMA_FLOPS_PER_TRIPLE_D[w] for w in which) * nominal_triples(c) * D * jobs
 
-    # ---------------- fwd-only and bwd-only timings (separate loops) ----------------
+    # ---------------- fwd-only and bwd-only timings (separate loops, this rank's problem) ----------------
     extra = {}
-    if c["bwd"]:
+    if c["bwd"] and args.mode == "bh":
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         torch.cuda.synchronize()
         e[0].record(stream)
@@ -449,46 +482,52 @@ def main():
         e[3].record(stream)
         torch.cuda.synchronize()
         fms, bms = e[0].elapsed_time(e[1]) / args.steps, e[2].elapsed_time(e[3]) / args.steps
-        extra = {"fwd_tflops": paper_flops(c, ("fwd",)) * world / (fms / 1e3) / 1e12,
-                 "bwd_tflops": paper_flops(c, ("bwd",)) * world / (bms / 1e3) / 1e12,
-                 "fwd_ms": fms, "bwd_ms": bms}
+        extra = {"fwd_tflops": paper_flops(cl, ("fwd",)) / (fms / 1e3) / 1e12,
+                 "bwd_tflops": paper_flops(cl, ("bwd",)) / (bms / 1e3) / 1e12,
+                 "fwd_ms": fms, "bwd_ms": bms, "per_rank": True}
 
     pk, pk_src = peaks()
-    peak_sust = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    peak_burst = pk["bf16_tflops"]
+    peak_sust = pk.get("bf16_tflops_sustained", peak_burst)
     mma_tflops = mma_flops_step * args.steps / (ms / 1e3) / 1e12
 
-    # ---------------- roofline of the dominant kernel ----------------
+    # ---------------- roofline of the dominant kernel (rank 0's live CUDA-event timing) ----------------
     roof = None
     if prof:
         dom = max(prof, key=lambda n: prof[n][0])
         tot_ms, cnt = prof[dom]
         avg_ms = tot_ms / cnt
-        w = kernel_work(dom, c, out_bytes)
+        w = kernel_work(dom, cl, out_bytes)
         step_share = tot_ms / ms if ms > 0 else None
         if w is not None:
-            bound, amount = w
+            bound, amount = w  # algorithmic work of this rank's problem per step
+            per_launch = amount * args.steps / cnt
             if bound == "tensor":
-                ach, unit, peak = amount / (avg_ms / 1e3) / 1e12, "TFLOP/s", peak_sust
+                # burst peak: the timed region is short (< 2 s at c3) and runs near the max SM clock
+                # (clocks below); the sustained figure was measured at a 1335 MHz power-capped clock
+                ach, unit, peak = per_launch / (avg_ms / 1e3) / 1e12, "TFLOP/s", peak_burst
             elif bound == "hbm":
-                ach, unit, peak = amount / (avg_ms / 1e3) / 1e9, "GB/s", pk["hbm_gbs"]
+                ach, unit, peak = per_launch / (avg_ms / 1e3) / 1e9, "GB/s", pk["hbm_gbs"]
             else:
-                ach, unit = amount / (avg_ms / 1e3) / 1e12, "TFLOP/s"
+                ach, unit = per_launch / (avg_ms / 1e3) / 1e12, "TFLOP/s"
                 peak = alu_peak_tflops(clk.get("sm_max_mhz") or 1965.0)
-            traffic, traffic_src = kernel_traffic(dom, c)
+            traffic, traffic_src = kernel_traffic(dom, c) if scaling == "weak" else (None, "not captured")
             roof = {"bound": bound, "kernel": dom, "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
-                    "algorithmic_per_launch": amount, "avg_launch_ms": avg_ms, "launches": cnt,
+                    "algorithmic_per_launch": per_launch, "avg_launch_ms": avg_ms, "launches": cnt,
                     "share_of_step": step_share,
-                    "peak_source": (f"{pk_src} MEASURED_PEAKS.json bf16_tflops_sustained" if bound == "tensor"
+                    "peak_source": (f"{pk_src} MEASURED_PEAKS.json bf16_tflops (burst)" if bound == "tensor"
                                     else f"{pk_src} hbm_gbs" if bound == "hbm"
                                     else "148 SM x 128 FP32 lanes x 2 x max SM clock")}
+            if bound == "tensor":
+                roof["frac_vs_sustained"] = ach / peak_sust
         roof_kernels = {n: {"ms_total": v[0], "launches": v[1]} for n, v in prof.items()}
     else:
         roof_kernels = {}
 
     # ---------------- end-to-end through the C ABI from pinned host buffers ----------------
     e2e = None
-    if not args.no_e2e and c["bwd"]:
+    if not args.no_e2e and c["bwd"] and args.mode == "bh":
         h_in = {n: x.pin_memory() for n, x in inp.items()}
         od = torch.float32 if args.out_f32 else torch.bfloat16
         h_out = {n: torch.empty(inp["q" if n in ("o", "dq") else "k"].shape, dtype=od).pin_memory()
@@ -529,19 +568,18 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": scaling, "vs_baseline": None,
             "dtype": "bf16", "compute": "bf16 inputs; fp16 MMA operands, fp32 accumulate (tcgen05) / fp32 (SIMT)",
             "data": "synthetic",
-            "config": config_block(c, world, args.mode),
+            "config": dict(config_block(c, world, args.mode, scaling), shard_rank0=shard_desc),
             "mma_basis_tflops": mma_tflops,
-            "pct_bf16_peak_mma_basis": 100.0 * mma_tflops / (peak_sust * world),
-            "pct_bf16_peak_paper_basis": 100.0 * value / (peak_sust * world),
+            "pct_bf16_peak_mma_basis": 100.0 * mma_tflops / (peak_burst * world),
             "paths": {"fwd": {1: "simt", 2: "tcgen05"}.get(fwd_path, fwd_path),
                       "bwd": {1: "simt", 2: "tcgen05"}.get(bwd_path, bwd_path)},
             **extra,
             "roofline": roof, "kernels": roof_kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-            "peaks": {"bf16_tflops": pk["bf16_tflops"], "bf16_tflops_sustained": peak_sust,
+            "peaks": {"bf16_tflops": peak_burst, "bf16_tflops_sustained": peak_sust,
                       "hbm_gbs": pk["hbm_gbs"], "source": pk_src},
         }
         print(json.dumps(line), flush=True)

@@ -25,19 +25,32 @@
  *   Input dtype (q,k,v,k2,v2,dO): bf16, or fp32 with SA_IN_F32.
  *   Output dtype (o, dq, dk, dv, dk2, dv2): fp32 if SA_OUT_F32 or SA_IN_F32, else bf16.
  *   The backward reads o in the output dtype.
- * OWNERSHIP.  The library allocates no device memory except the stream-ordered forward scratch of
- *   simplicial_attn_fwd / _prefixed (cudaMallocAsync/cudaFreeAsync on `stream`); simplicial_attn_fwd_ws
- *   and the backward take caller-provided workspaces (sizes from the *_workspace_bytes queries).
+ * OWNERSHIP.  The library never allocates device memory: forward and backward take caller-provided
+ *   workspaces (sizes from the *_workspace_bytes queries; a size of 0 allows a NULL workspace).
  *   Outputs must not alias inputs.
+ * KERNELS.  bf16 inputs run the tcgen05 (tensor-core) kernels, which need D in {64, 128} and a
+ *   folded window min(w1, w2) <= 128 (after clamping to n_prefix+N); any other bf16 call returns
+ *   SA_ERR_UNSUPPORTED -- there is no silent fallback.  fp32 inputs (SA_IN_F32) run the exact fp32
+ *   CUDA-core kernels (any D <= 128, any window); SA_FORCE_SIMT selects those for bf16 inputs too.
+ * INPUT RANGE (bf16 path).  The tensor-core kernels use fp16 MMA operands (reading R16):
+ *   q, k, v, k2, v2, dO are converted to fp16 and the row operands q o k2 and dO o v2 are formed in
+ *   fp16.  Finite results need |q_l k2_l| < 65504 and |dO_l v2_l| < 65504 for every l (e.g. all
+ *   |x| < 255), and inputs below 6.1e-5 in magnitude lose precision (fp16 subnormals).  Inputs
+ *   of unit scale -- the north star's workload -- sit far inside this range; larger or far
+ *   smaller activations should be rescaled by the caller or run with SA_IN_F32.  No check is made
+ *   (it would need a pass over the inputs).
  * EXECUTION.  Asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy default
  *   stream).  Results are valid after the caller synchronises.  Deterministic: no atomics on the
- *   data path, identical bits run to run.  Stateless and thread-safe (only cached driver entry
- *   points and a launch counter are global).
+ *   data path, identical bits run to run.  Re-entrant and thread-safe.  Global state: cached driver
+ *   entry points, a launch counter, the profiling registry (simplicial_attn_profile_*) and, per
+ *   device, the two copy streams of simplicial_attn_host_step, whose enqueue is serialised by a
+ *   per-device mutex.
  * ERRORS.  Returned synchronously before any launch: null pointers, B,H,N,D < 1, w1,w2 < 1,
- *   n_prefix < 0, DET with D < 3 -> SA_ERR_INVALID_ARG; D > 128 -> SA_ERR_UNSUPPORTED; workspace
- *   too small -> SA_ERR_WORKSPACE.  A window w > n_prefix+N is accepted and clamps.  Launch failures
- *   (cudaGetLastError) -> SA_ERR_CUDA.  Asynchronous faults surface at the caller's sync.  No C++
- *   exception crosses the ABI.
+ *   n_prefix < 0, DET with D < 3, unknown flag bits -> SA_ERR_INVALID_ARG; D > 128 or a bf16
+ *   shape the tensor-core kernels do not cover (see KERNELS) -> SA_ERR_UNSUPPORTED; workspace too
+ *   small (or NULL when nonzero bytes are needed) -> SA_ERR_WORKSPACE.  A window w > n_prefix+N is
+ *   accepted and clamps.  Launch failures (cudaGetLastError) -> SA_ERR_CUDA.  Asynchronous faults
+ *   surface at the caller's sync.  No C++ exception crosses the ABI.
  */
 #ifndef SIMPLICIAL_ATTN_H
 #define SIMPLICIAL_ATTN_H
@@ -67,30 +80,30 @@ enum {
 /* Kernel families the dispatcher can select (simplicial_attn_fwd_path / _bwd_path). */
 enum { SA_PATH_SIMT = 1, SA_PATH_TCGEN05 = 2 };
 
-/* Forward.  Writes o [B,N,H,D] and lse [B,H,N]. */
+/* Bytes of device workspace the forward needs (the tensor-core path keeps fp16 copies of q, k, v
+ * and the folded key there); 0 for the fp32 path.  The _prefixed form sizes it for n_prefix halo
+ * rows.  Returns 0 for invalid arguments as well. */
+size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                           int64_t w2, uint32_t flags);
+size_t simplicial_attn_fwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D,
+                                                    int64_t w1, int64_t w2, int64_t n_prefix,
+                                                    uint32_t flags);
+
+/* Forward (Alg. 1 P:255 with the windows of P:319-321).  Writes o [B,N,H,D] and
+ * lse [B,H,N].  workspace: simplicial_attn_fwd_workspace_bytes(...) bytes of device memory. */
 sa_status simplicial_attn_fwd(const void* q, const void* k, const void* v, const void* k2,
-                              const void* v2, void* o, float* lse, int64_t B, int64_t H, int64_t N,
-                              int64_t D, int64_t w1, int64_t w2, uint32_t flags, void* stream);
+                              const void* v2, void* o, float* lse, void* workspace,
+                              size_t workspace_bytes, int64_t B, int64_t H, int64_t N, int64_t D,
+                              int64_t w1, int64_t w2, uint32_t flags, void* stream);
 
 /* Sequence-sharded forward: k, v, k2, v2 carry n_prefix leading key-only rows
  * ([B, n_prefix+N, H, D]); query row i sits at key position n_prefix+i.  n_prefix = 0 is
- * simplicial_attn_fwd. */
+ * simplicial_attn_fwd.  Workspace from simplicial_attn_fwd_workspace_bytes_prefixed. */
 sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void* v, const void* k2,
-                                       const void* v2, void* o, float* lse, int64_t B, int64_t H,
-                                       int64_t N, int64_t D, int64_t w1, int64_t w2,
-                                       int64_t n_prefix, uint32_t flags, void* stream);
-
-/* Forward with a caller-provided device workspace (the bf16 tensor-core path keeps fp16 copies of
- * the long-window K and V there; the plain simplicial_attn_fwd takes that scratch stream-ordered
- * from cudaMallocAsync instead).  Size from simplicial_attn_fwd_workspace_bytes; 0 is valid for
- * paths that need none.  Otherwise identical to simplicial_attn_fwd_prefixed. */
-size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
-                                           int64_t w2, int64_t n_prefix, uint32_t flags);
-sa_status simplicial_attn_fwd_ws(const void* q, const void* k, const void* v, const void* k2,
-                                 const void* v2, void* o, float* lse, void* workspace,
-                                 size_t workspace_bytes, int64_t B, int64_t H, int64_t N, int64_t D,
-                                 int64_t w1, int64_t w2, int64_t n_prefix, uint32_t flags,
-                                 void* stream);
+                                       const void* v2, void* o, float* lse, void* workspace,
+                                       size_t workspace_bytes, int64_t B, int64_t H, int64_t N,
+                                       int64_t D, int64_t w1, int64_t w2, int64_t n_prefix,
+                                       uint32_t flags, void* stream);
 
 /* Bytes of device workspace the backward needs (delta_i [B,H,N] fp32, fp16 copies of the
  * key-side operands, band partials).  The _prefixed form sizes it for n_prefix halo rows. */

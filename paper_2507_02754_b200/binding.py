@@ -24,7 +24,7 @@ _STATUS = {0: "SA_OK", 1: "SA_ERR_INVALID_ARG", 2: "SA_ERR_UNSUPPORTED", 3: "SA_
            4: "SA_ERR_CUDA"}
 EXPORTS = (
     "simplicial_attn_fwd", "simplicial_attn_fwd_prefixed", "simplicial_attn_fwd_workspace_bytes",
-    "simplicial_attn_fwd_ws", "simplicial_attn_bwd_workspace_bytes",
+    "simplicial_attn_fwd_workspace_bytes_prefixed", "simplicial_attn_bwd_workspace_bytes",
     "simplicial_attn_bwd_workspace_bytes_prefixed",
     "simplicial_attn_bwd", "simplicial_attn_bwd_prefixed", "simplicial_attn_host_step_scratch_bytes",
     "simplicial_attn_host_step", "simplicial_attn_fwd_path", "simplicial_attn_bwd_path",
@@ -54,10 +54,10 @@ def load_library(build: bool = True):
     lib = ctypes.CDLL(path)
     P, I, U, S, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t, ctypes.c_float
     sig = {
-        "simplicial_attn_fwd": ([P] * 7 + [I] * 6 + [U, P], ctypes.c_int),
-        "simplicial_attn_fwd_prefixed": ([P] * 7 + [I] * 7 + [U, P], ctypes.c_int),
-        "simplicial_attn_fwd_workspace_bytes": ([I] * 7 + [U], S),
-        "simplicial_attn_fwd_ws": ([P] * 8 + [S] + [I] * 7 + [U, P], ctypes.c_int),
+        "simplicial_attn_fwd": ([P] * 8 + [S] + [I] * 6 + [U, P], ctypes.c_int),
+        "simplicial_attn_fwd_prefixed": ([P] * 8 + [S] + [I] * 7 + [U, P], ctypes.c_int),
+        "simplicial_attn_fwd_workspace_bytes": ([I] * 6 + [U], S),
+        "simplicial_attn_fwd_workspace_bytes_prefixed": ([I] * 7 + [U], S),
         "simplicial_attn_bwd_workspace_bytes": ([I] * 6 + [U], S),
         "simplicial_attn_bwd_workspace_bytes_prefixed": ([I] * 7 + [U], S),
         "simplicial_attn_bwd": ([P] * 14 + [S] + [I] * 6 + [U, P], ctypes.c_int),
@@ -182,10 +182,11 @@ def forward(q, k, v, k2, v2, w1: int, w2: int, det: bool = False, out_f32: bool 
                                        _ptr(ws), ws.numel(), B, H, h_kv, N, D, w1, w2, flags, _stream(q.device))
         _check(st, "simplicial_attn_fwd_gqa")
         return o, lse
-    wsb = int(L.simplicial_attn_fwd_workspace_bytes(B, H, N, D, w1, w2, n_prefix, flags))
+    wsb = int(L.simplicial_attn_fwd_workspace_bytes_prefixed(B, H, N, D, w1, w2, n_prefix, flags))
     ws = _workspace(q.device, wsb)
-    st = L.simplicial_attn_fwd_ws(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
-                                  _ptr(ws), ws.numel(), B, H, N, D, w1, w2, n_prefix, flags, _stream(q.device))
+    st = L.simplicial_attn_fwd_prefixed(_ptr(q), _ptr(k), _ptr(v), _ptr(k2), _ptr(v2), _ptr(o), _ptr(lse),
+                                        _ptr(ws), ws.numel(), B, H, N, D, w1, w2, n_prefix, flags,
+                                        _stream(q.device))
     _check(st, "simplicial_attn_fwd")
     return o, lse
 

@@ -71,8 +71,6 @@ cudaError_t simt_backward(const Problem& p, bool in_f32, bool out_f32, const voi
 // tcgen05 path (sa_tc_fwd.cu / sa_tc_bwd.cu)
 bool tc_fwd_supported(const Problem& p);
 size_t tc_fwd_workspace_bytes(const Problem& p);
-cudaError_t tc_forward(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
-                       const void* k2, const void* v2, void* o, float* lse, cudaStream_t st);
 cudaError_t tc_forward_ws(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
                           const void* k2, const void* v2, void* o, float* lse, void* ws, cudaStream_t st);
 bool tc_bwd_supported(const Problem& p);
@@ -134,6 +132,15 @@ static bool use_tc_bwd(const Problem& p, uint32_t flags) {
   return tc_bwd_supported(p);
 }
 
+// Kernel family for a call: fp32 inputs (SA_IN_F32) and the SA_FORCE_SIMT diagnostic take the exact
+// CUDA-core kernels; bf16 inputs take the tcgen05 kernels or are rejected (SA_ERR_UNSUPPORTED) --
+// there is no silent fallback to another backend.
+enum class Route { TC, SIMT, NONE };
+static Route route(const Problem& p, uint32_t flags, bool bwd) {
+  if (flags & (SA_IN_F32 | SA_FORCE_SIMT)) return Route::SIMT;
+  return (bwd ? tc_bwd_supported(p) : tc_fwd_supported(p)) ? Route::TC : Route::NONE;
+}
+
 static size_t bwd_ws(const Problem& p, uint32_t flags) {
   size_t base = align256(sizeof(float) * size_t(p.B) * p.H * p.N);  // delta
   if (use_tc_bwd(p, flags)) base += align256(tc_bwd_workspace_bytes(p));
@@ -152,9 +159,21 @@ using namespace sa;
 
 extern "C" {
 
-sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void* v, const void* k2,
-                                       const void* v2, void* o, float* lse, int64_t B, int64_t H,
-                                       int64_t N, int64_t D, int64_t w1, int64_t w2, int64_t n_prefix,
+size_t simplicial_attn_fwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
+                                                    int64_t w2, int64_t n_prefix, uint32_t flags) {
+  Problem p;
+  if (make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p) != SA_OK) return 0;
+  return use_tc_fwd(p, flags) ? tc_fwd_workspace_bytes(p) : 0;
+}
+
+size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
+                                           uint32_t flags) {
+  return simplicial_attn_fwd_workspace_bytes_prefixed(B, H, N, D, w1, w2, 0, flags);
+}
+
+sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void* v, const void* k2, const void* v2,
+                                       void* o, float* lse, void* workspace, size_t workspace_bytes, int64_t B,
+                                       int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2, int64_t n_prefix,
                                        uint32_t flags, void* stream) {
   if (!q || !k || !v || !k2 || !v2 || !o || !lse) return SA_ERR_INVALID_ARG;
   Problem p;
@@ -163,39 +182,22 @@ sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void*
   cudaStream_t st = (cudaStream_t)stream;
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   cudaGetLastError();  // clear stale errors so a failure below is ours
-  if (use_tc_fwd(p, flags)) return cuda_status(tc_forward(p, out_f32, q, k, v, k2, v2, o, lse, st));
-  return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
-}
-
-size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
-                                           int64_t n_prefix, uint32_t flags) {
-  Problem p;
-  if (make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p) != SA_OK) return 0;
-  return use_tc_fwd(p, flags) ? tc_fwd_workspace_bytes(p) : 0;
-}
-
-sa_status simplicial_attn_fwd_ws(const void* q, const void* k, const void* v, const void* k2, const void* v2,
-                                 void* o, float* lse, void* workspace, size_t workspace_bytes, int64_t B, int64_t H,
-                                 int64_t N, int64_t D, int64_t w1, int64_t w2, int64_t n_prefix, uint32_t flags,
-                                 void* stream) {
-  if (!q || !k || !v || !k2 || !v2 || !o || !lse) return SA_ERR_INVALID_ARG;
-  Problem p;
-  sa_status s = make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p);
-  if (s != SA_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
-  cudaGetLastError();
-  if (use_tc_fwd(p, flags)) {
-    if (!workspace || workspace_bytes < tc_fwd_workspace_bytes(p)) return SA_ERR_WORKSPACE;
-    return cuda_status(tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, workspace, st));
+  switch (route(p, flags, false)) {
+    case Route::TC:
+      if (!workspace || workspace_bytes < tc_fwd_workspace_bytes(p)) return SA_ERR_WORKSPACE;
+      return cuda_status(tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, workspace, st));
+    case Route::SIMT:
+      return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
+    default:
+      return SA_ERR_UNSUPPORTED;
   }
-  return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
 }
 
 sa_status simplicial_attn_fwd(const void* q, const void* k, const void* v, const void* k2, const void* v2,
-                              void* o, float* lse, int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
-                              int64_t w2, uint32_t flags, void* stream) {
-  return simplicial_attn_fwd_prefixed(q, k, v, k2, v2, o, lse, B, H, N, D, w1, w2, 0, flags, stream);
+                              void* o, float* lse, void* workspace, size_t workspace_bytes, int64_t B, int64_t H,
+                              int64_t N, int64_t D, int64_t w1, int64_t w2, uint32_t flags, void* stream) {
+  return simplicial_attn_fwd_prefixed(q, k, v, k2, v2, o, lse, workspace, workspace_bytes, B, H, N, D, w1, w2, 0,
+                                      flags, stream);
 }
 
 size_t simplicial_attn_bwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
@@ -221,16 +223,22 @@ sa_status simplicial_attn_bwd_prefixed(const void* q, const void* k, const void*
   Problem p;
   sa_status s = make_problem(B, H, N, D, w1, w2, n_prefix, flags, &p);
   if (s != SA_OK) return s;
+  if (route(p, flags, true) == Route::NONE) return SA_ERR_UNSUPPORTED;
   if (workspace_bytes < bwd_ws(p, flags)) return SA_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   float* delta = (float*)workspace;
   cudaGetLastError();
-  if (use_tc_bwd(p, flags))  // workspace: delta first, then the tcgen05 kernels' scratch
-    return cuda_status(tc_backward(p, out_f32, q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2,
-                                   workspace, workspace_bytes, st));
-  return cuda_status(simt_backward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2,
-                                   delta, st));
+  switch (route(p, flags, true)) {
+    case Route::TC:  // workspace: delta first, then the tcgen05 kernels' scratch
+      return cuda_status(tc_backward(p, out_f32, q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2, workspace,
+                                     workspace_bytes, st));
+    case Route::SIMT:
+      return cuda_status(simt_backward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2,
+                                       delta, st));
+    default:
+      return SA_ERR_UNSUPPORTED;
+  }
 }
 
 sa_status simplicial_attn_bwd(const void* q, const void* k, const void* v, const void* k2, const void* v2,
@@ -242,21 +250,24 @@ sa_status simplicial_attn_bwd(const void* q, const void* k, const void* v, const
                                       workspace_bytes, B, H, N, D, w1, w2, 0, flags, stream);
 }
 
-// Device scratch layout of the host step: 6 inputs | o | lse | 5 grads | bwd workspace.
-// Copy streams and events of the pipelined host step (one set per device, created on first use).
+// Device scratch layout of the host step: 6 inputs | o | lse | 5 grads | fwd/bwd workspace (shared:
+// the forward's scratch is dead once the backward starts on the same stream).
+// Copy streams and events of the pipelined host step: one set per device, created on first use and
+// guarded by a per-device mutex that simplicial_attn_host_step holds for its whole enqueue, so
+// concurrent calls on one device never re-record each other's events.
 struct HostPipe {
   bool ok = false;
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t entry = nullptr, out = nullptr;
   std::vector<cudaEvent_t> in, done;
+  std::mutex mu;
 };
-static HostPipe& host_pipe(int nchunks) {
-  static std::mutex mu;
+static HostPipe& host_pipe_of(int dev) {
   static HostPipe pipes[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> g(mu);
-  HostPipe& hp = pipes[dev & 63];
+  return pipes[dev & 63];
+}
+// Caller holds hp.mu.
+static bool host_pipe_reserve(HostPipe& hp, int nchunks) {
   if (!hp.h2d) {
     hp.ok = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
@@ -270,7 +281,7 @@ static HostPipe& host_pipe(int nchunks) {
     hp.in.push_back(a);
     hp.done.push_back(b);
   }
-  return hp;
+  return hp.ok;
 }
 
 static size_t host_step_layout(const Problem& p, uint32_t flags, size_t off[16]) {
@@ -282,7 +293,14 @@ static size_t host_step_layout(const Problem& p, uint32_t flags, size_t off[16])
   off[6] = cur; cur += align256(nel * eout);                               // o
   off[7] = cur; cur += align256(sizeof(float) * size_t(p.B) * p.H * p.N);  // lse
   for (int t = 8; t < 13; ++t) { off[t] = cur; cur += align256(nel * eout); }
-  off[13] = cur; cur += align256(bwd_ws(p, flags));
+  off[13] = cur;
+  {
+    size_t fw = 0;
+    Problem c = p;  // the step runs per chunk of (1, hc <= H) slices: size for the whole problem (an upper bound)
+    if (route(c, flags, false) == Route::TC) fw = tc_fwd_workspace_bytes(c);
+    const size_t bw = bwd_ws(p, flags);
+    cur += align256(fw > bw ? fw : bw);
+  }
   off[14] = cur;
   return cur;
 }
@@ -333,8 +351,11 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
   char* base = (char*)d_scratch;
   cudaStream_t st = (cudaStream_t)stream;
   cudaGetLastError();
-  HostPipe& hp = host_pipe(int(chunks.size()));
-  if (!hp.ok) return SA_ERR_CUDA;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  HostPipe& hp = host_pipe_of(dev);
+  std::lock_guard<std::mutex> lock(hp.mu);  // held for the whole enqueue (events are per call)
+  if (!host_pipe_reserve(hp, int(chunks.size()))) return SA_ERR_CUDA;
   cudaError_t e = cudaEventRecord(hp.entry, st);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.h2d, hp.entry, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.entry, 0);
@@ -361,7 +382,8 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.in[ci], 0);
     if (e != cudaSuccess) break;
     float* lse_c = (float*)(base + off[7]) + (c.b * H + c.h0) * N;
-    s = simplicial_attn_fwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, 1, c.hc, N, D, w1, w2, flags, stream);
+    s = simplicial_attn_fwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, base + off[13], off[14] - off[13], 1, c.hc,
+                            N, D, w1, w2, flags, stream);
     if (s != SA_OK) return s;
     s = simplicial_attn_bwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, P(5), P(8), P(9), P(10), P(11), P(12),
                             base + off[13], off[14] - off[13], 1, c.hc, N, D, w1, w2, flags, stream);
@@ -383,14 +405,16 @@ int simplicial_attn_fwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t
                              uint32_t flags) {
   Problem p;
   if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
-  return use_tc_fwd(p, flags) ? SA_PATH_TCGEN05 : SA_PATH_SIMT;
+  const Route r = route(p, flags, false);
+  return r == Route::TC ? SA_PATH_TCGEN05 : r == Route::SIMT ? SA_PATH_SIMT : 0;
 }
 
 int simplicial_attn_bwd_path(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1, int64_t w2,
                              uint32_t flags) {
   Problem p;
   if (make_problem(B, H, N, D, w1, w2, 0, flags, &p) != SA_OK) return 0;
-  return use_tc_bwd(p, flags) ? SA_PATH_TCGEN05 : SA_PATH_SIMT;
+  const Route r = route(p, flags, true);
+  return r == Route::TC ? SA_PATH_TCGEN05 : r == Route::SIMT ? SA_PATH_SIMT : 0;
 }
 
 uint64_t simplicial_attn_launch_count(void) { return g_launches.load(); }
@@ -511,11 +535,15 @@ sa_status simplicial_attn_fwd_gqa(const void* q, const void* k, const void* v, c
   cudaStream_t st = (cudaStream_t)stream;
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   cudaGetLastError();
-  if (use_tc_fwd(p, flags)) {
-    if (!workspace || workspace_bytes < tc_fwd_workspace_bytes(p)) return SA_ERR_WORKSPACE;
-    return cuda_status(tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, workspace, st));
+  switch (route(p, flags, false)) {
+    case Route::TC:
+      if (!workspace || workspace_bytes < tc_fwd_workspace_bytes(p)) return SA_ERR_WORKSPACE;
+      return cuda_status(tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, workspace, st));
+    case Route::SIMT:
+      return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
+    default:
+      return SA_ERR_UNSUPPORTED;
   }
-  return cuda_status(simt_forward(p, in_f32, out_f32, q, k, v, k2, v2, o, lse, st));
 }
 
 size_t simplicial_attn_bwd_gqa_workspace_bytes(int64_t B, int64_t H, int64_t H_kv, int64_t N, int64_t D,
@@ -541,6 +569,7 @@ sa_status simplicial_attn_bwd_gqa(const void* q, const void* k, const void* v, c
     return simplicial_attn_bwd(q, k, v, k2, v2, o, lse, dO, dq, dk, dv, dk2, dv2, workspace, workspace_bytes, B, H,
                                N, D, w1, w2, flags, stream);
   size_t off[8];
+  if (route(p, flags, true) == Route::NONE) return SA_ERR_UNSUPPORTED;
   if (workspace_bytes < gqa_bwd_layout(p, flags, off)) return SA_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   const bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
@@ -562,7 +591,7 @@ sa_status simplicial_attn_bwd_gqa(const void* q, const void* k, const void* v, c
   void* bw = w + off[6];
   const size_t bwb = off[7] - off[6];
   if (e == cudaSuccess) {
-    if (use_tc_bwd(p, flags32))
+    if (route(p, flags32, true) == Route::TC)
       e = tc_backward(p, true, q, k, v, k2, v2, o32, lse, dO, dq32, part[0], part[1], part[2], part[3], bw, bwb, st);
     else
       e = simt_backward(p, in_f32, true, q, k, v, k2, v2, o32, lse, dO, dq32, part[0], part[1], part[2], part[3],

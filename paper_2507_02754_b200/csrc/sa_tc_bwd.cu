@@ -79,7 +79,9 @@ struct BwdQArgs {
   void *dq, *dk2, *dv2;
   float* band;  // [grid][2 start/end][2 k2/v2][R-1][D]
   float* gring;  // R = 128 determinant: [grid][2 k2/v2][ring][D] fp32 ring, each CTA's own (no atomics)
-  int out_f32, R, lR, G, ngroups, items, per_cta, ring;
+  // R: rows per query of the tiling (a power of two >= the folded window Rt); rows with
+  // kk < R - Rt lie before the window and are masked like rows before the sequence start
+  int out_f32, R, lR, G, ngroups, items, per_cta, ring, Rt;
 };
 
 template <int D, int RING, bool STAGED>
@@ -1301,7 +1303,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool row_in = r < a.G * a.R && g < it.nq;
       const int pos = P0 + g;
       const int kpos = pos - a.R + 1 + kk;
-      const bool valid = row_in && kpos >= 0;
+      const bool valid = row_in && kpos >= 0 && kk >= a.R - a.Rt;
       float lse_l2 = 0.f, dl = 0.f;
       QRows rw{};
       if (row_in) {
@@ -1576,7 +1578,7 @@ struct BwdKVArgs {
   const __half *k, *v;             // fp16 copies of this kernel's stationary keys
   const float *lse, *delta;
   void *dk, *dv;
-  int out_f32, R, lR, G, ring;
+  int out_f32, R, lR, G, ring, Rt;  // R, Rt as in BwdQArgs
 };
 
 template <int D>
@@ -1708,7 +1710,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int g = r >> a.lR, kk = r & (a.R - 1);
         const int i = q0 + g;
         const int kpos = kbase + g + kk;
-        const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
+        const bool valid = r < a.G * a.R && i < qb && kpos >= 0 && kk >= a.R - a.Rt;
         float2 ri = make_float2(INFINITY, 0.f);
         if (valid) {
           if (STAGED) {
@@ -1929,7 +1931,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int g = r >> a.lR, kk = r & (a.R - 1);
         const int i = q0 + g;
         const int kpos = kbase + g + kk;
-        const bool valid = r < a.G * a.R && i < qb && kpos >= 0;
+        const bool valid = r < a.G * a.R && i < qb && kpos >= 0 && kk >= a.R - a.Rt;
         int slot = sbase + g + kk;
         if (slot >= a.ring) slot -= a.ring;
         const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
@@ -2129,7 +2131,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
       // fast path: the quarter's 32 columns belong to one query (R >= 32), no column is masked and no
       // row precedes the sequence start -> one (lse, delta) pair, packed math
-      const bool fast = all_in && a.R >= 32 && P0 - a.R + 1 >= 0;
+      const bool fast = all_in && a.R >= 32 && a.Rt == a.R && P0 - a.R + 1 >= 0;
       uint32_t su[32], du[32];
       tmem_ld32(tS, su);
       tmem_ld32(tdP, du);
@@ -2245,10 +2247,18 @@ cudaError_t simt_bwd_dk_only(const Problem& p, bool out_f32, const void* q, cons
 
 static bool swapped(const Problem& p) { return p.w1 < p.w2; }
 
+// Rows per query of the backward tiling: the folded window rounded up to a power of two (>= 2);
+// the extra leading rows of each query are masked (BwdQArgs::Rt).
+static int tile_rows(int w) {
+  int R = 2;
+  while (R < w) R <<= 1;
+  return R;
+}
+
 bool tc_bwd_supported(const Problem& p) {
   const int R = swapped(p) ? p.w1 : p.w2;
   if (!(p.D == 64 || p.D == 128)) return false;
-  return R >= 2 && R <= kMaxR && (R & (R - 1)) == 0;  // power-of-two rows per query
+  return R >= 1 && R <= kMaxR;
 }
 
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -2274,7 +2284,7 @@ static int q_grid(const Problem& p, int R, int G, int* per_cta, int* items_out) 
 size_t tc_bwd_workspace_bytes(const Problem& p0) {
   Problem p = p0;
   if (swapped(p)) std::swap(p.w1, p.w2);
-  const int R = p.w2, G = 128 / R;
+  const int R = tile_rows(p.w2), G = 128 / R;
   int pc, items;
   const int grid = q_grid(p, R, G, &pc, &items);
   const size_t n = p.nkey(), nq = size_t(p.B) * p.N * p.H * p.D;
@@ -2296,7 +2306,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     if (p.det) p.scale = -p.scale;
   }
   if (ws_bytes < tc_bwd_workspace_bytes(p0)) return cudaErrorInvalidValue;
-  const int R = p.w2, G = 128 / R;
+  const int Rt = p.w2, R = tile_rows(Rt), G = 128 / R;
   const size_t n = p.nkey();
   char* w = (char*)ws;
   float* delta = (float*)w;
@@ -2354,6 +2364,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.gring = gring;
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
+    a.Rt = Rt;
     a.lR = __builtin_ctz(unsigned(R));
     a.G = G;
     a.ngroups = (p.N + G - 1) / G;
@@ -2414,6 +2425,7 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.dv = dv;
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
+    a.Rt = Rt;
     a.lR = __builtin_ctz(unsigned(R));
     a.G = G;
     a.ring = R + 2 * G;

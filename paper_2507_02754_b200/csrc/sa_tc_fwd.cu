@@ -802,14 +802,4 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
   return cudaGetLastError();
 }
 
-cudaError_t tc_forward(const Problem& p, bool out_f32, const void* q, const void* k, const void* v, const void* k2,
-                       const void* v2, void* o, float* lse, cudaStream_t st) {
-  void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, tc_fwd_workspace_bytes(p), st);
-  if (e != cudaSuccess) return e;
-  e = tc_forward_ws(p, out_f32, q, k, v, k2, v2, o, lse, ws, st);
-  cudaError_t e2 = cudaFreeAsync(ws, st);
-  return e != cudaSuccess ? e : e2;
-}
-
 }  // namespace sa

@@ -11,6 +11,20 @@ TOL_F32 = 1e-4   # north star: fp32 path max abs error
 TOL_BF16 = 2e-2  # north star: bf16-in / fp32-accumulate path max abs error
 
 
+def record_errors(errs: dict, tol: float, tag: str | None = None) -> None:
+    """Print a parity test's worst max-abs error per tensor and append it to
+    gpurun_out/parity_errors.jsonl (when that directory exists: the GPU runs)."""
+    import json
+    import os
+    test = tag or os.environ.get("PYTEST_CURRENT_TEST", "?").split(" (")[0]
+    rec = {"test": test, "tol": tol, "max_abs": {n: float(e) for n, e in errs.items()}}
+    print("parity", json.dumps(rec))
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "parity_errors.jsonl"), "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
 def f64(t: torch.Tensor) -> np.ndarray:
     return t.detach().to("cpu", torch.float64).numpy()
 

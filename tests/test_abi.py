@@ -49,25 +49,37 @@ def test_argument_validation_without_gpu(lib):
     null = ctypes.c_void_p(0)
     f = lib.simplicial_attn_fwd
     ok_args = lambda **kw: [kw.get(n, fake) for n in ("q", "k", "v", "k2", "v2", "o", "lse")]
+    big = 1 << 40
     # null pointer
-    assert f(*ok_args(q=null), 1, 1, 8, 16, 4, 2, 0, null) == 1
+    assert f(*ok_args(q=null), fake, big, 1, 1, 8, 16, 4, 2, 0, null) == 1
     # bad sizes / windows
-    assert f(*ok_args(), 0, 1, 8, 16, 4, 2, 0, null) == 1
-    assert f(*ok_args(), 1, 1, 8, 16, 0, 2, 0, null) == 1
-    assert f(*ok_args(), 1, 1, 8, 16, 4, -1, 0, null) == 1
+    assert f(*ok_args(), fake, big, 0, 1, 8, 16, 4, 2, 0, null) == 1
+    assert f(*ok_args(), fake, big, 1, 1, 8, 16, 0, 2, 0, null) == 1
+    assert f(*ok_args(), fake, big, 1, 1, 8, 16, 4, -1, 0, null) == 1
     # DET needs D >= 3; D > 128 unsupported; unknown flag bits rejected
-    assert f(*ok_args(), 1, 1, 8, 2, 4, 2, 1, null) == 1
-    assert f(*ok_args(), 1, 1, 8, 256, 4, 2, 0, null) == 2
-    assert f(*ok_args(), 1, 1, 8, 16, 4, 2, 1 << 9, null) == 1
+    assert f(*ok_args(), fake, big, 1, 1, 8, 2, 4, 2, 1, null) == 1
+    assert f(*ok_args(), fake, big, 1, 1, 8, 256, 4, 2, 0, null) == 2
+    assert f(*ok_args(), fake, big, 1, 1, 8, 16, 4, 2, 1 << 9, null) == 1
     # prefixed: negative prefix
-    assert lib.simplicial_attn_fwd_prefixed(*ok_args(), 1, 1, 8, 16, 4, 2, -1, 0, null) == 1
+    assert lib.simplicial_attn_fwd_prefixed(*ok_args(), fake, big, 1, 1, 8, 16, 4, 2, -1, 0, null) == 1
+    # bf16 inputs with no tensor-core kernel for the shape: rejected, never a silent CUDA-core run
+    assert f(*ok_args(), fake, big, 1, 1, 8, 16, 4, 2, 0, null) == 2          # D = 16
+    assert f(*ok_args(), fake, big, 1, 1, 512, 64, 256, 200, 0, null) == 2   # both windows > 128
+    # forward workspace: the tensor-core path needs one; too small / NULL is rejected
+    fws = lib.simplicial_attn_fwd_workspace_bytes(1, 2, 64, 128, 32, 8, 0)
+    assert fws >= 3 * 2 * 64 * 128 * 2
+    assert lib.simplicial_attn_fwd_workspace_bytes_prefixed(1, 2, 64, 128, 32, 8, 7, 0) > fws
+    assert f(*ok_args(), fake, fws - 1, 1, 2, 64, 128, 32, 8, 0, null) == 3
+    assert f(*ok_args(), null, fws, 1, 2, 64, 128, 32, 8, 0, null) == 3
+    assert lib.simplicial_attn_fwd_workspace_bytes(1, 1, 128, 16, 32, 8, 2) == 0  # fp32 path: none
     # backward: workspace too small
-    ws = lib.simplicial_attn_bwd_workspace_bytes(1, 2, 64, 16, 8, 4, 0)
+    ws = lib.simplicial_attn_bwd_workspace_bytes(1, 2, 64, 16, 8, 4, 2)
     assert ws >= 4 * 2 * 64
     b = lib.simplicial_attn_bwd
     args = [fake] * 14
-    assert b(*args, ws - 1, 1, 2, 64, 16, 8, 4, 0, null) == 3
-    assert lib.simplicial_attn_host_step_scratch_bytes(1, 2, 64, 16, 8, 4, 0) > 0
+    assert b(*args, ws - 1, 1, 2, 64, 16, 8, 4, 2, null) == 3
+    assert b(*args, 1 << 40, 1, 2, 64, 16, 8, 4, 0, null) == 2  # bf16, D = 16
+    assert lib.simplicial_attn_host_step_scratch_bytes(1, 2, 64, 16, 8, 4, 2) > 0
 
 
 def test_path_selection(lib):
@@ -75,6 +87,16 @@ def test_path_selection(lib):
     assert lib.simplicial_attn_fwd_path(1, 1, 128, 16, 32, 8, 2) == 1
     assert lib.simplicial_attn_fwd_path(1, 1, 128, 16, 32, 8, 1 << 3) == 1
     assert lib.simplicial_attn_fwd_path(1, 1, 128, 300, 32, 8, 0) == 0
+    # bf16: tensor cores or nothing (SA_FORCE_SIMT is the only way onto the CUDA-core kernels)
+    for fn in (lib.simplicial_attn_fwd_path, lib.simplicial_attn_bwd_path):
+        assert fn(4, 16, 8192, 128, 512, 32, 0) == 2
+        assert fn(2, 16, 16384, 128, 512, 32, 1) == 2
+        assert fn(1, 1, 256, 128, 40, 64, 0) == 2     # folded window 40: not a power of two
+        assert fn(1, 1, 256, 128, 64, 1, 0) == 2      # w2 = 1
+        assert fn(1, 1, 256, 64, 200, 128, 1) == 2
+        assert fn(1, 1, 256, 48, 64, 32, 0) == 0      # D = 48: no tcgen05 kernel
+        assert fn(1, 1, 512, 128, 256, 200, 0) == 0   # both windows > 128
+        assert fn(1, 1, 256, 48, 64, 32, 1 << 3) == 1
 
 
 def test_product_path_does_not_touch_oracle():

@@ -51,9 +51,12 @@ def _worker(rank, world, port, data, w1, w2, det, out):
 
 
 @pytest.mark.parametrize("det", [False, True])
-@pytest.mark.parametrize("w1,w2", [(7, 3), (4, 9)])
-def test_sequence_sharded_matches_unsharded(oracle_mod, det, w1, w2):
-    world = 2
+@pytest.mark.parametrize("world,w1,w2", [
+    (2, 7, 3),   # interior queries computed while the halo is in flight (L=12 > halo 6)
+    (2, 4, 9),   # w2 > w1: the K'/V' halo is the longer one
+    (3, 9, 2),   # L = 8 = halo: no interior queries; the middle rank sends and receives
+])
+def test_sequence_sharded_matches_unsharded(oracle_mod, det, world, w1, w2):
     rng = np.random.default_rng(5)
     B, N, H, D = 1, 24, 2, 6
     data = {n: rng.standard_normal((B, N, H, D)) for n in ("q", "k", "v", "k2", "v2", "dO")}
@@ -85,3 +88,14 @@ def test_seq_shard_rejects_short_shards():
     with pytest.raises(ValueError):
         parallel.seq_shard(64, 1, 8, n_halo=15)
     assert parallel.seq_shard(64, 1, 4, n_halo=15) == (16, 32, 15)
+    with pytest.raises(ValueError):
+        parallel._check_lengths(7, 9, 2, world=2)  # queries would need rank r-2's rows
+    assert parallel._check_lengths(8, 9, 2, world=2) == 8
+
+
+def test_bh_slice_blocks():
+    assert parallel.bh_slice(8, 32, 3, 8) == (3, 4, 0, 32)     # c5 at 8 GPUs: one batch element each
+    assert parallel.bh_slice(8, 32, 1, 2) == (4, 8, 0, 32)
+    assert parallel.bh_slice(4, 16, 5, 8) == (2, 3, 8, 16)     # c3 at 8 GPUs: half the heads of one b
+    with pytest.raises(ValueError):
+        parallel.bh_slice(3, 4, 1, 2)                           # [6, 12) spans b = 1 and 2 partially

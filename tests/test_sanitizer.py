@@ -1,0 +1,37 @@
+"""compute-sanitizer over small runs of every tensor-core kernel variant (tools/sanitize_run.py):
+memcheck (out-of-bounds / misaligned global and shared accesses), racecheck (shared-memory data
+races: the named-barrier handoffs and the rotated dK'/dV' ring of tc_bwd_q) and synccheck
+(barrier misuse).  The method itself has no atomics; these check that the kernels' own
+synchronisation is sound.  Each tool must report 0 errors."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    from paper_2507_02754_b200 import binding
+    binding.load_library()  # build before the sanitized process starts
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "17", "--print-limit", "20"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "all"]
+    cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    log = r.stdout + r.stderr
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, f"sanitizer_{tool}.log"), "w") as f:
+            f.write(" ".join(cmd) + "\n" + log)
+    m = re.search(r"ERROR SUMMARY: (\d+) error", log)
+    assert r.returncode == 0 and m is not None and int(m.group(1)) == 0, log[-4000:]
+    assert log.count(" ok") >= 8, log[-2000:]
