@@ -1593,7 +1593,9 @@ struct KVSmem {
   alignas(16) __half sdo[2][kKVGmax][D];
   float slse[2][kKVGmax], sdl[2][kKVGmax];
   float2 rinfo[2][128];  // (lse * log2e or +inf for invalid rows, delta)
-  uint64_t kvtm, aready[2], afree[2], sfull[2], pready[2], done;
+  // rready/rfree: direct former -> softmax handoff of rinfo[buf] (every former / softmax thread
+  // arrives), so the row info does not rely on ordering carried through the MMA warp's commits
+  uint64_t kvtm, aready[2], afree[2], sfull[2], pready[2], rready[2], rfree[2], done;
   uint32_t tmem_base;
 };
 
@@ -1629,6 +1631,8 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_init(&sm.afree[s], 1);
       mbar_init(&sm.sfull[s], 1);
       mbar_init(&sm.pready[s], 4);
+      mbar_init(&sm.rready[s], 32 * kKVFW);
+      mbar_init(&sm.rfree[s], 32 * 8);
     }
     mbar_init(&sm.done, 1);
     fence_mbar_init();
@@ -1702,6 +1706,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         named_bar_sync(2, kNF);
       }
       mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
+      mbar_wait(&sm.rfree[buf], ((t >> 1) & 1) ^ 1);  // softmax warps are done with rinfo[buf] of tile t-2
       SA_TRACE_AT(trf, 3, trn, t << 16 | 31 << 8);
       // row info: (lse * log2e, delta), +inf marks rows outside the problem
       const int kbase = p.np + q0 - a.R + 1;  // key row of tile row 0
@@ -1722,6 +1727,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
         sm.rinfo[buf][r] = ri;
       }
+      mbar_arrive(&sm.rready[buf]);
       SA_TRACE_AT(trf, 3, trn, t << 16 | 33 << 8);
       // A_S = q o k2 [det: k2 x q], A_dP = dO o v2 -> swizzled fp16 tiles
       constexpr int kWS = DET ? 24 : 8;       // A_S task width (elements)
@@ -2125,6 +2131,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const bool trs = (threadIdx.x & 127) == 0 && t >= 50 && t < 53;
       mbar_wait(&sm.sfull[wg], (Q >> 1) & 1);
       tc_fence_after();
+      if (q < 2) mbar_wait(&sm.rready[buf], (t >> 1) & 1);  // first quarter of tile t for this warpgroup
       SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (50 + q) << 8);
       // column c (tile row) belongs to query g = c / R at position P0 + g; key row j is in its window
       // iff P0 + g - w1 < j <= P0 + g  <=>  g in [j - P0, j - P0 + w1 - 1]
@@ -2173,6 +2180,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         }
       }
       SA_TRACE_AT(trs, 5 + wg, trn, t << 16 | (64 + q) << 8);
+      if (q >= 2) mbar_arrive(&sm.rfree[buf]);  // last read of rinfo[buf] for tile t by this warpgroup
       tmem_st16(tS, pp);
       tmem_st16(tdP, pd);
       tmem_st_wait();
