@@ -18,6 +18,7 @@
 //            dS^T on the CUDA cores, dV += P^T A_dP, dK += dS^T A_S (TS-MMA).
 // Row operands: A_S = s (q o k2)  [det: s (k2 x q)],  A_dP = dO o v2, fp16; K, V fp16 copies.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <utility>
@@ -2249,6 +2250,13 @@ __global__ void __launch_bounds__(kKVThreads, 1)
 
 }  // namespace
 
+bool tc_bwd_q2_supported(const Problem& p, int R, int Rt);
+int tc_bwd_q2_pairs(const Problem& p, int R, int G, int* per_pair, int* items_out);
+cudaError_t tc_bwd_q2_launch(const Problem& p, bool out_f32, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                             const __half* q, const __half* k2, const __half* v2, const __half* dO, const float* lse,
+                             const float* delta, void* dq, void* dk2, void* dv2, float* band, int R, int G,
+                             cudaStream_t st);
+
 cudaError_t simt_bwd_dk_only(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
                              const void* k2, const void* v2, const void* dO, const float* lse, const float* delta,
                              void* dk, void* dv, cudaStream_t st);
@@ -2377,6 +2385,23 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.G = G;
     a.ngroups = (p.N + G - 1) / G;
     a.ring = R + G;
+    // The CTA-pair kernel (sa_tc_bwdq2.cu) is an opt-in experiment (SA_BWDQ_PAIR=1): it measured
+    // 17.1 ms against 11.0 ms for tc_bwd_q at c3.  Both write the same band layout,
+    // so the fold is shared.
+    static const bool pair = getenv("SA_BWDQ_PAIR") && atoi(getenv("SA_BWDQ_PAIR")) != 0;
+    if (pair && tc_bwd_q2_supported(p, R, Rt)) {
+      const int pairs = tc_bwd_q2_pairs(p, R, G, &a.per_cta, &a.items);
+      e = tc_bwd_q2_launch(p, out_f32, tmK, tmV, a.q, a.k2, a.v2, a.dO, lse, delta, dq, dk2, dv2, band, R, G, st);
+      if (e != cudaSuccess) return e;
+      KernelScope ks("tc_fold", st);
+      const int fb = std::max(1, pairs - 1);
+      if (out_f32)
+        fold_kernel<float><<<fb, 256, 0, st>>>(a, pairs);
+      else
+        fold_kernel<__nv_bfloat16><<<fb, 256, 0, st>>>(a, pairs);
+      goto kv;
+    }
+    {
     const int grid = q_grid(p, R, G, &a.per_cta, &a.items);
     auto launch = [&](auto kern, size_t smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -2413,7 +2438,9 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
       fold_kernel<float><<<fb, 256, 0, st>>>(a, grid);
     else
       fold_kernel<__nv_bfloat16><<<fb, 256, 0, st>>>(a, grid);
+    }
   }
+kv:
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
