@@ -306,6 +306,14 @@ def run_membound(args, c):
     e[2].record(stream)
     torch.cuda.synchronize()
     fms, bms = e[0].elapsed_time(e[1]) / steps, e[1].elapsed_time(e[2]) / steps
+    # per-kernel split of one more fwd+bwd (library CUDA-event profiling)
+    sa.profile_read()
+    sa.profile_enable(True)
+    o, lse = sa.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], w1, w2)
+    sa.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], w1, w2)
+    torch.cuda.synchronize()
+    kern = {n: round(v[0], 3) for n, v in sa.profile_read().items()}
+    sa.profile_enable(False)
     rows = B * H * N
     fb, bb = rows * (12 * D + 4), rows * (24 * D + 8)
     pk, src = peaks()
@@ -318,6 +326,7 @@ def run_membound(args, c):
         "tflops_paper_basis": paper_flops(cc) / ((fms + bms) / 1e3) / 1e12,
         "paths": {"fwd": {1: "simt", 2: "tcgen05"}.get(sa.fwd_path(B, H, N, D, w1, w2)),
                   "bwd": {1: "simt", 2: "tcgen05"}.get(sa.bwd_path(B, H, N, D, w1, w2))},
+        "kernels_ms": kern,
     }), flush=True)
 
 

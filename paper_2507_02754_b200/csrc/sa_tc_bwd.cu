@@ -917,6 +917,143 @@ __device__ __forceinline__ void q_epilogue_pass_det(QSmem<D, RING, STAGED>& sm, 
   named_bar_sync(1, kQNT);
 }
 
+// Half SUB of the determinant row operand k2 x q (3-chunks, fp32 math, fp16 packed): columns
+// [D/2 SUB, D/2 SUB + D/2), computing every 3-chunk that overlaps them (compile-time column indices,
+// so the packed row stays in registers).  Columns past the last whole chunk are 0 (reading R5).
+template <int D, int SUB>
+__device__ __forceinline__ void det_half_operand(const __half* x, const __half* y, uint32_t (&pk)[D / 4]) {
+  constexpr int DH = D / 2, D3 = (D / 3) * 3, C0 = DH * SUB, CH0 = C0 / 3;
+#pragma unroll
+  for (int cc = 0; cc < (DH + 2) / 3 + 1; ++cc) {
+    constexpr int kDummy = 0;
+    (void)kDummy;
+    const int e0 = 3 * (CH0 + cc);
+    if (e0 < C0 + DH && e0 + 3 <= D3) {
+      float xf[3], yf[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        xf[u] = __half2float(x[e0 + u]);
+        yf[u] = __half2float(y[e0 + u]);
+      }
+      // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
+      const float av[3] = {yf[1] * xf[2] - yf[2] * xf[1], yf[2] * xf[0] - yf[0] * xf[2], yf[0] * xf[1] - yf[1] * xf[0]};
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int col = e0 + u - C0;
+        if (col >= 0 && col < DH) {
+          const uint32_t h = uint32_t(__half_as_ushort(__float2half_rn(av[u])));
+          pk[col >> 1] |= (col & 1) ? (h << 16) : h;
+        }
+      }
+    }
+  }
+}
+
+// Determinant epilogue at R = 32 (G = 4 queries, one per TMEM lane quarter), row-owned like
+// q_epilogue_rot: six 24-column blocks (eight 3-chunks each; the last holds chunks 40-41 and the two
+// trailing columns), warp m = 2 half + sub of a lane quarter takes 6 columns (two chunks) of a block.
+// Query g works on block (ph + g) mod 6 in phase ph, so rows of different queries that share a key
+// row never update the same ring columns in the same phase; one barrier per phase.  Per thread:
+//   dq  (register reduce-scatter over the query's 32 rows)  s sum_k W x k2
+//   dk2 ring row += s q x W,   dv2 ring row += dO o U      (cross products chunkwise, reading R5:
+//   the D mod 3 trailing columns get no dq / dk2, but their dv2 = dO o U)
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_rot_det(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                                   int half, int sub, int r, bool valid, const QRows& rw,
+                                                   uint32_t tW, uint32_t tU, int sbase) {
+  constexpr int D3 = (D / 3) * 3;
+  constexpr int kNB = (D + 23) / 24;  // 24-column blocks
+  const Problem& p = a.p;
+  const float s = p.scale;
+  const int ln = r & 31, g = r >> 5;
+  const int m = 2 * half + sub;
+  int slot = sbase + (r & 31) + g;  // key row P0 - 31 + g + kk
+  if (slot >= a.ring) slot -= a.ring;
+  auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
+#pragma unroll 1
+  for (int ph = 0; ph < kNB; ++ph) {
+    int b = ph + g;
+    if (b >= kNB) b -= kNB;
+    const int cs = 24 * b + 6 * m;
+    const bool act = cs < D;  // warp-uniform
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = 0.f;
+    if (act) {
+      uint32_t uw[8], uu[8];
+      tmem_ld8(tW + cs, uw);
+      tmem_ld8(tU + cs, uu);
+      float k2v[6], qv[6], dov[6];
+#pragma unroll
+      for (int e = 0; e < 6; ++e) k2v[e] = qv[e] = dov[e] = 0.f;
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 6; e += 2) {
+          if (cs + e < D) {
+            const float2 a2 = __half22float2(*reinterpret_cast<const __half2*>(rw.k2 + cs + e));
+            const float2 b2 = __half22float2(*reinterpret_cast<const __half2*>(rw.q + cs + e));
+            const float2 c2 = __half22float2(*reinterpret_cast<const __half2*>(rw.dO + cs + e));
+            k2v[e] = a2.x, k2v[e + 1] = a2.y, qv[e] = b2.x, qv[e + 1] = b2.y, dov[e] = c2.x, dov[e + 1] = c2.y;
+          }
+        }
+      }
+      tmem_ld_wait();
+      float w[6], ck[6], cv[6];
+#pragma unroll
+      for (int e = 0; e < 6; ++e) {
+        w[e] = __uint_as_float(uw[e]);
+        ck[e] = 0.f;
+        cv[e] = cs + e < D ? dov[e] * __uint_as_float(uu[e]) : 0.f;
+      }
+#pragma unroll
+      for (int t = 0; t < 6; t += 3) {
+        if (cs + t + 3 <= D3) {  // dq: W x k2 ; dk2: q x W     ((x cross y)_r = x_{r+1} y_{r+2} - x_{r+2} y_{r+1})
+          v[t + 0] = s * (w[t + 1] * k2v[t + 2] - w[t + 2] * k2v[t + 1]);
+          v[t + 1] = s * (w[t + 2] * k2v[t + 0] - w[t + 0] * k2v[t + 2]);
+          v[t + 2] = s * (w[t + 0] * k2v[t + 1] - w[t + 1] * k2v[t + 0]);
+          ck[t + 0] = s * (qv[t + 1] * w[t + 2] - qv[t + 2] * w[t + 1]);
+          ck[t + 1] = s * (qv[t + 2] * w[t + 0] - qv[t + 0] * w[t + 2]);
+          ck[t + 2] = s * (qv[t + 0] * w[t + 1] - qv[t + 1] * w[t + 0]);
+        }
+      }
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 6; e += 2) {
+          if (cs + e < D) {
+            float2* pk = reinterpret_cast<float2*>(&ak[slot][cs + e]);
+            float2* pv = reinterpret_cast<float2*>(&av[slot][cs + e]);
+            float2 xk = *pk, xv = *pv;
+            xk.x += ck[e], xk.y += ck[e + 1], xv.x += cv[e], xv.y += cv[e + 1];
+            *pk = xk;
+            *pv = xv;
+          }
+        }
+      }
+    }
+    // reduce-scatter the 8 (six real) dq columns over the query's 32 lanes
+#pragma unroll
+    for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+      const bool hi = ln & st;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+      }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+    if (act && (ln & 3) == 0 && col < 6 && cs + col < D && g < it.nq) {
+      const int64_t off = p.qoff(it.b, it.i0 + g, it.h) + cs + col;
+      if (a.out_f32)
+        reinterpret_cast<float*>(a.dq)[off] = v[0];
+      else
+        reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+    }
+    named_bar_sync(1, kQNT);
+  }
+}
+
 template <int D, bool DET, int RING, bool STAGED>
 __global__ void __launch_bounds__(kQThreads, 1)
     tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
@@ -1194,52 +1331,23 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool tr = (threadIdx.x & 127) == 0 && threadIdx.x < 256 && fitem - it_begin >= 100 && fitem - it_begin < 102;
       const int treg = 1 + half;
         if (DET && half == 0) {
-          uint32_t pk[D / 2];
+          // A_S = k2 x q chunkwise; sub-warp `sub` writes columns [D/2 sub, D/2 sub + D/2) and computes
+          // the 3-chunks that overlap them (the chunk straddling D/2 is computed by both)
+          constexpr int DH = D / 2;
+          constexpr int D3 = (D / 3) * 3;
+          uint32_t pk[DH / 2];
   #pragma unroll
-          for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
-          if (fvalid && sub == 0) {
-            const __half* x = fr.q;
-            const __half* y = fr.k2;
-            {
-              constexpr int D3 = (D / 3) * 3;
-  #pragma unroll
-              for (int base = 0; base < D; base += 24) {
-                float xf[24], yf[24];
-  #pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                  if (base + 8 * u < D) {
-                    float tx[8], ty[8];
-                    load_f16<8>(x + base + 8 * u, tx);
-                    load_f16<8>(y + base + 8 * u, ty);
-  #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                      xf[8 * u + e] = tx[e];
-                      yf[8 * u + e] = ty[e];
-                    }
-                  } else {
-  #pragma unroll
-                    for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
-                  }
-                }
-  #pragma unroll
-                for (int c3 = 0; c3 < 24; c3 += 3) {
-                  float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-                  if (base + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
-                    a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
-                    a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
-                    a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
-                  }
-                  xf[c3] = a0;
-                  xf[c3 + 1] = a1;
-                  xf[c3 + 2] = a2;
-                }
-  #pragma unroll
-                for (int e = 0; e < 24; e += 2)
-                  if (base + e < D) pk[(base + e) / 2] = pack_f16x2(xf[e], xf[e + 1]);
-              }
-            }
+          for (int t = 0; t < DH / 2; ++t) pk[t] = 0u;
+          if (fvalid) {
+            if (sub == 0)
+              det_half_operand<D, 0>(fr.q, fr.k2, pk);
+            else
+              det_half_operand<D, 1>(fr.q, fr.k2, pk);
           }
-          if (sub == 0) tmem_store_row<D>(tAS, pk);
+          if constexpr (DH == 64)
+            tmem_st32(tAS + (DH / 2) * sub, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+          else
+            tmem_st16(tAS + (DH / 2) * sub, pk);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
@@ -1415,6 +1523,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
           else
             reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
         }
+      } else if constexpr (Sm::kRot && DET) {
+        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        q_epilogue_rot_det<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
       } else if constexpr (Sm::kRot) {
         const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
         q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase, tr, treg, trn,
@@ -2412,10 +2523,11 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     const bool staged = G <= 16 && 2 * G + 2 * (R + G - 1) <= kQStageRows && R + G <= 36;
     const bool gr = R + G > kRingMax;  // R = 128: the ring lives in the global slab
 #define SA_Q_LAUNCH(DD, DET, RING, STG) launch(tc_bwd_q_kernel<DD, DET, RING, STG>, sizeof(QSmem<DD, RING, STG>) + 1024)
-    const bool rot = !p.det && p.D == 128 && (R == 32 || R == 64);  // row-owned epilogue, 4 K/V stages
+    // row-owned epilogue, 4 K/V stages: trilinear R = 32 / 64, determinant R = 32 (q_epilogue_rot_det)
+    const bool rot = p.D == 128 && (R == 32 || (!p.det && R == 64));
 #define SA_Q_PICK(DD, DET)                                                                             \
   (gr ? SA_Q_LAUNCH(DD, DET, DET ? 129 : 130, false)                                                  \
-      : (!DET && DD == 128 && rot) ? (staged ? SA_Q_LAUNCH(DD, DET, 37, true) : SA_Q_LAUNCH(DD, DET, 67, false)) \
+      : (DD == 128 && rot) ? (staged ? SA_Q_LAUNCH(DD, DET, 37, true) : SA_Q_LAUNCH(DD, DET, 67, false)) \
       : staged ? SA_Q_LAUNCH(DD, DET, 36, true) : SA_Q_LAUNCH(DD, DET, 66, false))
     if (p.D == 128) {
       if (p.det)
