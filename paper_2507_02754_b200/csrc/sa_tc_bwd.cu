@@ -83,6 +83,7 @@ struct BwdQArgs {
   // R: rows per query of the tiling (a power of two >= the folded window Rt); rows with
   // kk < R - Rt lie before the window and are masked like rows before the sequence start
   int out_f32, R, lR, G, ngroups, items, per_cta, ring, Rt;
+  FastDiv fd_ng, fd_H, fd_ring;  // by ngroups, H, ring (per-tile index arithmetic)
 };
 
 template <int D, int RING, bool STAGED>
@@ -146,10 +147,10 @@ struct QItem {
 
 __device__ __forceinline__ QItem q_item(const BwdQArgs& a, int item) {
   QItem it;
-  it.bh = item / a.ngroups;
-  it.grp = item % a.ngroups;
-  it.b = it.bh / a.p.H;
-  it.h = it.bh % a.p.H;
+  it.bh = a.fd_ng.div(item);
+  it.grp = item - it.bh * a.ngroups;
+  it.b = a.fd_H.div(it.bh);
+  it.h = it.bh - it.b * a.p.H;
   it.hk = a.p.hk(it.h);
   it.i0 = it.grp * a.G;
   it.nq = min(a.G, a.p.N - it.i0);
@@ -315,7 +316,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
   // dk2 / dv2: key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g)
   const int P0 = p.np + it.i0;
   const int nsl = a.R + it.nq - 1;
-  const int sbase = (P0 - a.R + 1 + a.ring) % a.ring;
+  const int sbase = a.fd_ring.mod(P0 - a.R + 1 + a.ring);
   for (int idx = tid256; idx < nsl * PW; idx += kQNT) {
     const int sl = idx / PW, d = idx % PW;
     const int kp = P0 - a.R + 1 + sl;
@@ -1234,7 +1235,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const QItem it = q_item(a, item);
         const int P0 = p.np + it.i0;
         const bool fresh = item == it_begin || it.grp == 0;  // first item of a (b,h) run: whole window
-        const int rh = (it.bh - it_begin / a.ngroups) & 1;
+        const int rh = (it.bh - a.fd_ng.div(it_begin)) & 1;
         const int klo = fresh ? P0 - a.R + 1 : P0;
         const int nkn = P0 + a.G - klo;  // key rows to stage
         const int nrows = 2 * a.G + 2 * nkn;
@@ -1311,7 +1312,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (fvalid) {
         const int nk = a.R + a.G - 1;
         if constexpr (Sm::kRing) {
-          const int rh = (fi.bh - it_begin / a.ngroups) & 1;
+          const int rh = (fi.bh - a.fd_ng.div(it_begin)) & 1;
           fr.q = &sm.stgq[bf][g][0];
           fr.dO = &sm.stgq[bf][a.G + g][0];
           fr.k2 = &sm.rk2[rh][fkpos % Sm::kKR][0];
@@ -1428,7 +1429,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (valid) {
         const int nk = a.R + a.G - 1;
         if constexpr (Sm::kRing) {
-          const int rh = (it.bh - it_begin / a.ngroups) & 1;
+          const int rh = (it.bh - a.fd_ng.div(it_begin)) & 1;
           rw.q = &sm.stgq[buf][g][0];
           rw.dO = &sm.stgq[buf][a.G + g][0];
           rw.k2 = &sm.rk2[rh][kpos % Sm::kKR][0];
@@ -1510,7 +1511,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       tc_fence_after();
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 5 << 8);
       if constexpr (Sm::kG1) {
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32)
           q_epilogue_g1<D, RING, STAGED>(sm, a, c0, half, sub, r, valid, rw, tW, tU, sbase);
@@ -1524,10 +1525,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
             reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
         }
       } else if constexpr (Sm::kRot && DET) {
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
         q_epilogue_rot_det<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
       } else if constexpr (Sm::kRot) {
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
         q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase, tr, treg, trn,
                                         item - it_begin);
         if (a.R == 64 && tid256 < 2 * D) {  // dq = the two lane quarters' partials of each query
@@ -1542,7 +1543,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           }
         }
       } else if (DET && (a.R == 32 || a.R == 64)) {
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 24)
           q_epilogue_pass_det<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
@@ -1555,14 +1556,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
                                                         sub == 0);
       } else if (a.R == 32 || a.R == 64) {
 #pragma unroll 1
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
         for (int c0 = 0; c0 < D; c0 += 32) {
           q_epilogue_pass32<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
           SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | (c0 / 32));
         }
       } else if (a.R >= 2 && a.R < 32) {
 #pragma unroll 1
-        const int sbase = (p.np + it.i0 - a.R + 1 + a.ring) % a.ring;
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
         for (int c0 = 0; c0 < D; c0 += 32) {
           q_epilogue_pass_small<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
           SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | (c0 / 32));
@@ -1579,7 +1580,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool end_open = last_in_sub && PE < p.np + p.N;
       const bool start_open = PS > p.np;
       const int nrows = flush_hi - flush_lo + 1;
-      const int fbase = (flush_lo + a.ring) % a.ring;
+      const int fbase = a.fd_ring.mod(flush_lo + a.ring);
       for (int idx = tid256; idx < nrows * D; idx += kQNT) {
         const int kp = flush_lo + idx / D, d = idx % D;
         if (kp < 0 || kp >= p.NK()) continue;
@@ -1691,6 +1692,7 @@ struct BwdKVArgs {
   const float *lse, *delta;
   void *dk, *dv;
   int out_f32, R, lR, G, ring, Rt;  // R, Rt as in BwdQArgs
+  FastDiv fd_ring;
 };
 
 template <int D>
@@ -1761,7 +1763,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
     constexpr int kNF = 32 * kKVFW;
     // stage tile t's new rows (K2/V2 ring rows, q/dO rows, lse/delta) with cp.async
     auto ring_mod = [&](int kp) {  // kp mod ring for kp >= -ring (one division per call site)
-      return (kp + a.ring) % a.ring;
+      return a.fd_ring.mod(kp + a.ring);
     };
     auto stage = [&](int t) {
       const int q0 = qa + t * a.G, P0 = p.np + q0;
@@ -1885,60 +1887,87 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
         }
         if (DET) {
-          // A_S = k2 x q (chunkwise cross products; trailing D mod 3 dims 0): tasks (row, 24-column
-          // block), kTS blocks per row, spread over all former threads
+          // A_S = k2 x q (chunkwise cross products; trailing D mod 3 dims 0): tasks (row pair (r, r+1)
+          // of one query, 24-column block).  The query's q block is converted once for both rows and
+          // the two rows' cross products run as packed fp32x2 arithmetic (FMUL2 / FFMA2).
           constexpr int D3 = (D / 3) * 3;
-          for (int task = ft; task < 128 * kTS; task += kNF) {
-            const int r = task / kTS, e0 = (task % kTS) * 24;
+          constexpr int kNBlk = (D + 23) / 24;
+          for (int task = ft; task < 64 * kNBlk; task += kNF) {
+            const int rp = task / kNBlk, e0 = (task - rp * kNBlk) * 24;
+            const int r = 2 * rp;  // rows r, r+1 (R even: same query)
             const int g2 = r >> a.lR, kk2 = r & (a.R - 1);
-            const bool ok = r < a.G * a.R && q0 + g2 < qb && kbase + g2 + kk2 >= 0;
-            uint32_t pk[12];
+            const bool qok = r < a.G * a.R && q0 + g2 < qb;
+            const bool ok0 = qok && kbase + g2 + kk2 >= 0, ok1 = qok && kbase + g2 + kk2 + 1 >= 0;
+            uint32_t pk0[12], pk1[12];
 #pragma unroll
-            for (int e = 0; e < 12; ++e) pk[e] = 0u;
-            if (ok) {
+            for (int e = 0; e < 12; ++e) pk0[e] = pk1[e] = 0u;
+            if (ok0 || ok1) {
               int sl = sbase + g2 + kk2;
               if (sl >= a.ring) sl -= a.ring;
-              float xf[24], yf[24];
+              int sl1 = sl + 1;
+              if (sl1 >= a.ring) sl1 -= a.ring;
+              float xf[24];
+              float2 yf[24];  // (row r, row r+1) pairs of k2
 #pragma unroll
               for (int u = 0; u < 3; ++u) {
                 if (e0 + 8 * u < D) {
                   const uint4 xv = *reinterpret_cast<const uint4*>(&sm.sq[buf][g2][e0 + 8 * u]);
-                  const uint4 yv = *reinterpret_cast<const uint4*>(&sm.rk2[sl][e0 + 8 * u]);
-                  const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+                  const uint4 y0 = ok0 ? *reinterpret_cast<const uint4*>(&sm.rk2[sl][e0 + 8 * u]) : make_uint4(0u, 0u, 0u, 0u);
+                  const uint4 y1 = ok1 ? *reinterpret_cast<const uint4*>(&sm.rk2[sl1][e0 + 8 * u]) : make_uint4(0u, 0u, 0u, 0u);
+                  const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, a0[4] = {y0.x, y0.y, y0.z, y0.w},
+                                 a1[4] = {y1.x, y1.y, y1.z, y1.w};
 #pragma unroll
                   for (int e = 0; e < 4; ++e) {
                     const float2 fx = __half22float2(*reinterpret_cast<const __half2*>(&xs[e]));
-                    const float2 fy = __half22float2(*reinterpret_cast<const __half2*>(&ys[e]));
+                    const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&a0[e]));
+                    const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&a1[e]));
                     xf[8 * u + 2 * e] = fx.x;
                     xf[8 * u + 2 * e + 1] = fx.y;
-                    yf[8 * u + 2 * e] = fy.x;
-                    yf[8 * u + 2 * e + 1] = fy.y;
+                    yf[8 * u + 2 * e] = make_float2(f0.x, f1.x);
+                    yf[8 * u + 2 * e + 1] = make_float2(f0.y, f1.y);
                   }
                 } else {
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) xf[8 * u + e] = yf[8 * u + e] = 0.f;
+                  for (int e = 0; e < 8; ++e) {
+                    xf[8 * u + e] = 0.f;
+                    yf[8 * u + e] = make_float2(0.f, 0.f);
+                  }
                 }
               }
 #pragma unroll
               for (int c3 = 0; c3 < 24; c3 += 3) {
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-                if (e0 + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
-                  a0 = yf[c3 + 1] * xf[c3 + 2] - yf[c3 + 2] * xf[c3 + 1];
-                  a1 = yf[c3 + 2] * xf[c3 + 0] - yf[c3 + 0] * xf[c3 + 2];
-                  a2 = yf[c3 + 0] * xf[c3 + 1] - yf[c3 + 1] * xf[c3 + 0];
+                float2 r0 = make_float2(0.f, 0.f), r1 = r0, r2 = r0;
+                if (e0 + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}, both rows at once
+                  const float2 q0 = make_float2(xf[c3], xf[c3]), q1 = make_float2(xf[c3 + 1], xf[c3 + 1]),
+                               q2 = make_float2(xf[c3 + 2], xf[c3 + 2]);
+                  r0 = ffma2(yf[c3 + 1], q2, fmul2(yf[c3 + 2], make_float2(-q1.x, -q1.y)));
+                  r1 = ffma2(yf[c3 + 2], q0, fmul2(yf[c3 + 0], make_float2(-q2.x, -q2.y)));
+                  r2 = ffma2(yf[c3 + 0], q1, fmul2(yf[c3 + 1], make_float2(-q0.x, -q0.y)));
                 }
-                xf[c3] = a0;
-                xf[c3 + 1] = a1;
-                xf[c3 + 2] = a2;
+                yf[c3] = r0;
+                yf[c3 + 1] = r1;
+                yf[c3 + 2] = r2;
               }
 #pragma unroll
-              for (int e = 0; e < 12; ++e) pk[e] = pack_f16x2(xf[2 * e], xf[2 * e + 1]);
+              for (int e = 0; e < 12; ++e) {
+                pk0[e] = pack_f16x2(yf[2 * e].x, yf[2 * e + 1].x);
+                pk1[e] = pack_f16x2(yf[2 * e].y, yf[2 * e + 1].y);
+              }
+              if (!ok0)
+#pragma unroll
+                for (int e = 0; e < 12; ++e) pk0[e] = 0u;
+              if (!ok1)
+#pragma unroll
+                for (int e = 0; e < 12; ++e) pk1[e] = 0u;
             }
 #pragma unroll
             for (int u = 0; u < 3; ++u)
-              if (e0 + 8 * u < D)
+              if (e0 + 8 * u < D) {
                 *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r, e0 / 8 + u)) =
-                    make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+                    make_uint4(pk0[4 * u], pk0[4 * u + 1], pk0[4 * u + 2], pk0[4 * u + 3]);
+                *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r + 1, e0 / 8 + u)) =
+                    make_uint4(pk1[4 * u], pk1[4 * u + 1], pk1[4 * u + 2], pk1[4 * u + 3]);
+              }
           }
         }
         SA_TRACE_AT(trf, 3, trn, t << 16 | 34 << 8);
@@ -2496,6 +2525,9 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     a.G = G;
     a.ngroups = (p.N + G - 1) / G;
     a.ring = R + G;
+    a.fd_ng = FastDiv(a.ngroups);
+    a.fd_H = FastDiv(p.H);
+    a.fd_ring = FastDiv(a.ring);
     // The CTA-pair kernel (sa_tc_bwdq2.cu) is an opt-in experiment (SA_BWDQ_PAIR=1): it measured
     // 17.1 ms against 11.0 ms for tc_bwd_q at c3.  Both write the same band layout,
     // so the fold is shared.
@@ -2576,6 +2608,7 @@ kv:
     a.lR = __builtin_ctz(unsigned(R));
     a.G = G;
     a.ring = R + 2 * G;
+    a.fd_ring = FastDiv(a.ring);
     const bool staged = G <= kKVGmax && a.ring <= kKVRing;
     dim3 grid((p.NK() + 127) / 128, p.B * p.H);
     auto launch = [&](auto kern, size_t smem) {
