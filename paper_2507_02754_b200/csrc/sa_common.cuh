@@ -39,18 +39,22 @@ struct Problem {
 
 // Division by a runtime divisor 1 <= d < 2^31 for 0 <= n < 2^31 by a host-computed reciprocal:
 // q = mulhi(n, ceil(2^32 / d)) is q or q+1, one correction step makes it exact.  A few instructions
-// instead of the ~25 of an integer division on the kernels' per-tile index paths.
+// instead of the ~25 of an integer division on the kernels' per-tile index paths.  d = 1 (whose
+// reciprocal 2^32 does not fit 32 bits) is a separate, warp-uniform branch.
 struct FastDiv {
   int d;
   uint32_t m;
   FastDiv() = default;
-  __host__ explicit FastDiv(int d_) : d(d_), m(uint32_t((0x100000000ull + uint64_t(d_) - 1) / uint64_t(d_))) {}
+  __host__ explicit FastDiv(int d_)
+      : d(d_), m(d_ > 1 ? uint32_t((0x100000000ull + uint64_t(d_) - 1) / uint64_t(d_)) : 0u) {}
   __device__ __forceinline__ int div(int n) const {
+    if (d == 1) return n;
     int q = int(__umulhi(uint32_t(n), m));
     if (n - q * d < 0) --q;
     return q;
   }
   __device__ __forceinline__ int mod(int n) const {
+    if (d == 1) return 0;
     int r = n - int(__umulhi(uint32_t(n), m)) * d;
     if (r < 0) r += d;
     return r;
