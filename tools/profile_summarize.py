@@ -8,7 +8,7 @@ import csv, io, json, os, shutil, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("SA_PROF_DIR", os.path.join(ROOT, "profiles"))
 
 
 def raw_metrics(rep):
@@ -23,10 +23,10 @@ def to_bytes(v, unit):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-def main(tag):
+def main(tag, prefix="", cfg="c3"):
     traffic = {}
     for k in ("tc_fwd", "tc_bwd_q", "tc_bwd_kv"):
-        rep = os.path.join(OUT, f"full_{k}.ncu-rep")
+        rep = os.path.join(OUT, f"{prefix}full_{k}.ncu-rep")
         if not os.path.exists(rep):
             continue
         d, u = raw_metrics(rep)
@@ -38,21 +38,25 @@ def main(tag):
                       "ncu_duration_ms": t_ns / 1e6,
                       "tensor_pipe_pct": next((float(v) for kk, v in d.items() if kk.endswith(
                           "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")), None),
-                      "report": f"gpurun_out/full_{k}.ncu-rep (not committed; summary in {tag}_ncu_{k}.txt)"}
+                      "report": f"gpurun_out/{prefix}full_{k}.ncu-rep (not committed; summary in {tag}_{prefix}ncu_{k}.txt)"}
         txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep],
                              capture_output=True, text=True).stdout
         lines = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, "30"],
                                capture_output=True, text=True).stdout
-        with open(os.path.join(PROF, f"{tag}_ncu_{k}.txt"), "w") as f:
+        with open(os.path.join(PROF, f"{tag}_{prefix}ncu_{k}.txt"), "w") as f:
             f.write(txt + "\n== per-CUDA-line warp stall samples (tools/ncu_lines.py)\n" + lines)
-    with open(os.path.join(PROF, f"{tag}_traffic_c3.json"), "w") as f:
-        json.dump({"config": "c3", "capture": "ncu --set full --clock-control none, one launch each, bench.py "
-                   "--steps 1 --warmup 1", "kernels": traffic}, f, indent=1)
+    if not traffic:
+        return
+    with open(os.path.join(PROF, f"{tag}_traffic_{cfg}.json"), "w") as f:
+        json.dump({"config": cfg, "capture": "ncu --set full --clock-control none, one launch each, bench.py "
+                   + ("--sweep membound" if prefix else "") + " --steps 1 --warmup 1", "kernels": traffic}, f, indent=1)
     src = os.path.join(OUT, "launches_c3.csv")
-    if os.path.exists(src):
+    if not prefix and os.path.exists(src):
         shutil.copy(src, os.path.join(PROF, f"{tag}_launches_c3.csv"))
     print(json.dumps(traffic, indent=1))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    main(tag)
+    main(tag, prefix="mb_", cfg="membound")
