@@ -120,6 +120,9 @@ struct QSmem {
   static constexpr int kKR = 40;  // ring slots per half (>= R + 2G - 1 = 39)
   alignas(16) __half stg[(STAGED && !kRing) ? 2 : 1][(STAGED && !kRing) ? kQStageRows : 1][D + 8];
   alignas(16) __half stgq[kRing ? 2 : 1][kRing ? 8 : 1][D + 8];  // q rows 0..G-1, dO rows G..2G-1
+  // the same rows in fp32 (q pre-multiplied by s) for the epilogue: converted once per tile instead
+  // of once per use by each of the query's 32 rows
+  alignas(16) float stgqf[kRing ? 2 : 1][kRing ? 8 : 1][kRing ? D : 4];
   alignas(16) __half rk2[kRing ? 2 : 1][kRing ? kKR : 1][D + 8];
   alignas(16) __half rv2[kRing ? 2 : 1][kRing ? kKR : 1][D + 8];
   float slse[2][16], sdl[2][16];
@@ -160,6 +163,26 @@ __device__ __forceinline__ QItem q_item(const BwdQArgs& a, int item) {
   it.nch = (it.span + kQChunk - 1) / kQChunk;
   return it;
 }
+// The item after `it` in the flat (b, h, group) order, without divisions (items of a CTA are contiguous).
+__device__ __forceinline__ QItem q_item_next(const BwdQArgs& a, const QItem& it) {
+  QItem n = it;
+  if (++n.grp == a.ngroups) {
+    n.grp = 0;
+    ++n.bh;
+    if (++n.h == a.p.H) {
+      n.h = 0;
+      ++n.b;
+    }
+    n.hk = a.p.hk(n.h);
+  }
+  n.i0 = n.grp * a.G;
+  n.nq = min(a.G, a.p.N - n.i0);
+  const int pos0 = a.p.np + n.i0, posl = pos0 + n.nq - 1;
+  n.jbeg = max(0, pos0 - a.p.w1 + 1);
+  n.span = posl - n.jbeg + 1;
+  n.nch = (n.span + kQChunk - 1) / kQChunk;
+  return n;
+}
 __device__ __forceinline__ int q_width(const QItem& it, int c) {
   if (c < it.nch - 1) return kQChunk;
   return ((it.span - kQChunk * (it.nch - 1)) + 15) & ~15;
@@ -183,6 +206,7 @@ __device__ __forceinline__ void load_f16(const __half* p, float (&f)[N]) {
 // Row sources of the current tile: staged shared-memory rows or the global fp16 copies.
 struct QRows {
   const __half *q, *dO, *k2, *v2;  // this thread's rows (valid rows only)
+  const float *qf, *dOf;           // RING 37: fp32 copies of the q (pre-scaled by s) and dO rows
 };
 
 // One epilogue pass over columns [c0, c0+PW) of the tile's W (half 0) / U (half 1) rows:
@@ -535,21 +559,30 @@ __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const
   const int ln = r & 31, qd = r >> 5;
   const int g = r >> a.lR;
   const int m = 2 * half + sub;
-  const int rot = g * (4 / a.G);
+  const int rot = g << (a.lR - 5);  // g * R / 32 = g * 4 / G (R = 32: g, R = 64: 2g)
   int slot = sbase + (r & (a.R - 1)) + g;  // key row P0 - R + 1 + g + kk
   if (slot >= a.ring) slot -= a.ring;
   auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
   // operands of phase ph+1 (TMEM W/U columns, fp16 row chunks) are requested before phase ph's
   // reduction and barrier, so their latency overlaps them
+  constexpr bool kF = QSmem<D, RING, STAGED>::kRing;  // fp32 q (x s) / dO rows staged
   uint32_t uw[8], uu[8];
   uint4 rk2 = make_uint4(0u, 0u, 0u, 0u), rq = rk2, rdo = rk2;
+  float4 fq0 = make_float4(0.f, 0.f, 0.f, 0.f), fq1 = fq0, fd0 = fq0, fd1 = fq0;
   int cs = 32 * (rot & 3) + 8 * m;
   tmem_ld8(tW + cs, uw);
   tmem_ld8(tU + cs, uu);
   if (valid) {
     rk2 = *reinterpret_cast<const uint4*>(rw.k2 + cs);
-    rq = *reinterpret_cast<const uint4*>(rw.q + cs);
-    rdo = *reinterpret_cast<const uint4*>(rw.dO + cs);
+    if constexpr (kF) {
+      fq0 = *reinterpret_cast<const float4*>(rw.qf + cs);
+      fq1 = *reinterpret_cast<const float4*>(rw.qf + cs + 4);
+      fd0 = *reinterpret_cast<const float4*>(rw.dOf + cs);
+      fd1 = *reinterpret_cast<const float4*>(rw.dOf + cs + 4);
+    } else {
+      rq = *reinterpret_cast<const uint4*>(rw.q + cs);
+      rdo = *reinterpret_cast<const uint4*>(rw.dO + cs);
+    }
   }
 #pragma unroll
   for (int ph = 0; ph < 4; ++ph) {
@@ -565,18 +598,27 @@ __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const
     {
       const uint32_t ks[4] = {rk2.x, rk2.y, rk2.z, rk2.w}, qs[4] = {rq.x, rq.y, rq.z, rq.w},
                      ds[4] = {rdo.x, rdo.y, rdo.z, rdo.w};
+      const float fq[8] = {fq0.x, fq0.y, fq0.z, fq0.w, fq1.x, fq1.y, fq1.z, fq1.w};
+      const float fd[8] = {fd0.x, fd0.y, fd0.z, fd0.w, fd1.x, fd1.y, fd1.z, fd1.w};
 #pragma unroll
       for (int e2 = 0; e2 < 4; ++e2) {
         const float2 kf = __half22float2(*reinterpret_cast<const __half2*>(&ks[e2]));
-        const float2 qf = __half22float2(*reinterpret_cast<const __half2*>(&qs[e2]));
-        const float2 df = __half22float2(*reinterpret_cast<const __half2*>(&ds[e2]));
         const float w0 = __uint_as_float(uw[2 * e2]), w1 = __uint_as_float(uw[2 * e2 + 1]);
         v[2 * e2] = s * kf.x * w0;
         v[2 * e2 + 1] = s * kf.y * w1;
-        ck[2 * e2] = s * qf.x * w0;
-        ck[2 * e2 + 1] = s * qf.y * w1;
-        cv[2 * e2] = df.x * __uint_as_float(uu[2 * e2]);
-        cv[2 * e2 + 1] = df.y * __uint_as_float(uu[2 * e2 + 1]);
+        if constexpr (kF) {
+          ck[2 * e2] = fq[2 * e2] * w0;
+          ck[2 * e2 + 1] = fq[2 * e2 + 1] * w1;
+          cv[2 * e2] = fd[2 * e2] * __uint_as_float(uu[2 * e2]);
+          cv[2 * e2 + 1] = fd[2 * e2 + 1] * __uint_as_float(uu[2 * e2 + 1]);
+        } else {
+          const float2 qf = __half22float2(*reinterpret_cast<const __half2*>(&qs[e2]));
+          const float2 df = __half22float2(*reinterpret_cast<const __half2*>(&ds[e2]));
+          ck[2 * e2] = s * qf.x * w0;
+          ck[2 * e2 + 1] = s * qf.y * w1;
+          cv[2 * e2] = df.x * __uint_as_float(uu[2 * e2]);
+          cv[2 * e2 + 1] = df.y * __uint_as_float(uu[2 * e2 + 1]);
+        }
       }
     }
     if (valid) {
@@ -597,8 +639,15 @@ __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const
       tmem_ld8(tU + cs, uu);
       if (valid) {
         rk2 = *reinterpret_cast<const uint4*>(rw.k2 + cs);
-        rq = *reinterpret_cast<const uint4*>(rw.q + cs);
-        rdo = *reinterpret_cast<const uint4*>(rw.dO + cs);
+        if constexpr (kF) {
+          fq0 = *reinterpret_cast<const float4*>(rw.qf + cs);
+          fq1 = *reinterpret_cast<const float4*>(rw.qf + cs + 4);
+          fd0 = *reinterpret_cast<const float4*>(rw.dOf + cs);
+          fd1 = *reinterpret_cast<const float4*>(rw.dOf + cs + 4);
+        } else {
+          rq = *reinterpret_cast<const uint4*>(rw.q + cs);
+          rdo = *reinterpret_cast<const uint4*>(rw.dO + cs);
+        }
       }
     }
 #pragma unroll
@@ -1099,8 +1148,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       uint32_t kc = 0;
-      for (int item = it_begin; item < it_end; ++item) {
-        QItem it = q_item(a, item);
+      QItem it = it_begin < it_end ? q_item(a, it_begin) : QItem{};
+      for (int item = it_begin; item < it_end; ++item, it = q_item_next(a, it)) {
         for (int c = 0; c < it.nch; ++c, ++kc) {
           const int s = kc % kStages;
           const uint32_t ph = (kc / kStages) & 1;
@@ -1122,8 +1171,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
       uint32_t kc = 0, gc = 0;
       int trn = 0;
-      for (int item = it_begin; item < it_end; ++item) {
-        QItem it = q_item(a, item);
+      QItem it = it_begin < it_end ? q_item(a, it_begin) : QItem{};
+      for (int item = it_begin; item < it_end; ++item, it = q_item_next(a, it)) {
         const bool trm = lane == 0 && item - it_begin >= 100 && item - it_begin < 102;
         named_bar_sync(4, kQNT + 32);  // A operands formed (all compute warps bar.arrive)
         SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | 10 << 8);
@@ -1208,10 +1257,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
     const uint32_t tAS = tbase + kQAS + lane_off, tAdP = tbase + kQAdP + lane_off;
     const Problem& p = a.p;
     const float sl2 = p.scale * kLog2e;
+    const int bh_begin = a.fd_ng.div(it_begin);  // (b,h) of the CTA's first tile
     // stage tile `item`'s rows into buffer `buf` (cp.async, one group per call)
-    auto stage = [&](int item, int buf) {
+    auto stage = [&](const QItem& it, int item, int buf) {
       if (!STAGED) {  // no shared-memory staging (large R): pull the next tile's rows into L2 instead
-        const QItem it = q_item(a, item);
         const int P0 = p.np + it.i0;
         const int nk = a.R + a.G - 1;
         constexpr int kLines = D * 2 / 128;  // 128-byte lines per fp16 row
@@ -1232,10 +1281,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
         return;
       }
       if constexpr (Sm::kRing) {
-        const QItem it = q_item(a, item);
         const int P0 = p.np + it.i0;
         const bool fresh = item == it_begin || it.grp == 0;  // first item of a (b,h) run: whole window
-        const int rh = (it.bh - a.fd_ng.div(it_begin)) & 1;
+        const int rh = (it.bh - bh_begin) & 1;
         const int klo = fresh ? P0 - a.R + 1 : P0;
         const int nkn = P0 + a.G - klo;  // key rows to stage
         const int nrows = 2 * a.G + 2 * nkn;
@@ -1267,7 +1315,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
         cp_async_commit();
         return;
       }
-      const QItem it = q_item(a, item);
       const int P0 = p.np + it.i0;
       const int nk = a.R + a.G - 1;
       const int nrows = 2 * a.G + 2 * nk;
@@ -1302,8 +1349,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     //      half 1 -> A_dP = dO o v2, from staging buffer `bf`.  Formed for tile t+1 right after the
     //      chunk loop of tile t (the A regions are free then), so the S/dP MMAs of t+1 overlap the
     //      epilogue of t. ----
-    auto form_A = [&](int fitem, int bf) {
-      const QItem fi = q_item(a, fitem);
+    auto form_A = [&](const QItem& fi, int fitem, int bf) {
       const int fP0 = p.np + fi.i0;
       const int g = r >> a.lR, kk = r & (a.R - 1);
       const int fkpos = fP0 + g - a.R + 1 + kk;
@@ -1312,7 +1358,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (fvalid) {
         const int nk = a.R + a.G - 1;
         if constexpr (Sm::kRing) {
-          const int rh = (fi.bh - a.fd_ng.div(it_begin)) & 1;
+          const int rh = (fi.bh - bh_begin) & 1;
           fr.q = &sm.stgq[bf][g][0];
           fr.dO = &sm.stgq[bf][a.G + g][0];
           fr.k2 = &sm.rk2[rh][fkpos % Sm::kKR][0];
@@ -1385,22 +1431,34 @@ __global__ void __launch_bounds__(kQThreads, 1)
           SA_TRACE_AT(tr, treg, trn, (fitem - it_begin) << 16 | 2 << 8);
         }
     };
+    // RING 37: fp32 copies (q x s, dO) of the staged q / dO rows of buffer `bf` for the epilogue
+    auto cvt_qf = [&](int bf) {
+      if constexpr (Sm::kRing) {
+        for (int idx = tid256; idx < 2 * a.G * D; idx += kQNT) {
+          const int row = idx / D, col = idx - row * D;
+          sm.stgqf[bf][row][col] = __half2float(sm.stgq[bf][row][col]) * (row < a.G ? p.scale : 1.f);
+        }
+      }
+    };
+    QItem itc = it_begin < it_end ? q_item(a, it_begin) : QItem{};  // tile of the current iteration
     if (it_begin < it_end) {
-      stage(it_begin, 0);
+      stage(itc, it_begin, 0);
       if (STAGED) {
         cp_async_wait<0>();
         named_bar_sync(1, kQNT);
       }
-      form_A(it_begin, 0);
+      cvt_qf(0);
+      form_A(itc, it_begin, 0);
     }
     for (int item = it_begin; item < it_end; ++item) {
-      QItem it = q_item(a, item);
+      const QItem it = itc;
+      const QItem itn = q_item_next(a, it);  // the next tile (no division)
       const bool tr = (threadIdx.x & 127) == 0 && threadIdx.x < 256 && item - it_begin >= 100 && item - it_begin < 102;
       const int treg = 1 + half;
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 1 << 8);
       const int buf = STAGED ? int(gc & 1) : 0;
       // this tile's rows were staged (and waited for) before its A operands were formed; prefetch the next
-      if (item + 1 < it_end) stage(item + 1, STAGED ? (buf ^ 1) : 0);
+      if (item + 1 < it_end) stage(itn, item + 1, STAGED ? (buf ^ 1) : 0);
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 8 << 8);
       const bool first_in_sub = item == it_begin || it.grp == 0;
       const bool last_in_sub = item == it_end - 1 || it.grp == a.ngroups - 1;
@@ -1429,9 +1487,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (valid) {
         const int nk = a.R + a.G - 1;
         if constexpr (Sm::kRing) {
-          const int rh = (it.bh - a.fd_ng.div(it_begin)) & 1;
+          const int rh = (it.bh - bh_begin) & 1;
           rw.q = &sm.stgq[buf][g][0];
           rw.dO = &sm.stgq[buf][a.G + g][0];
+          rw.qf = &sm.stgqf[buf][g][0];
+          rw.dOf = &sm.stgqf[buf][a.G + g][0];
           rw.k2 = &sm.rk2[rh][kpos % Sm::kKR][0];
           rw.v2 = &sm.rv2[rh][kpos % Sm::kKR][0];
         } else if (STAGED) {
@@ -1504,7 +1564,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (item + 1 < it_end) {
         if (STAGED) cp_async_wait<0>();
         named_bar_sync(1, kQNT);  // every warp is past its last S/dP wait: the A regions are free
-        form_A(item + 1, STAGED ? (buf ^ 1) : 0);
+        cvt_qf(buf ^ 1);
+        form_A(itn, item + 1, STAGED ? (buf ^ 1) : 0);
       }
       // ---- epilogue ----
       mbar_wait(&sm.udone, gc & 1);
@@ -1616,6 +1677,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 7 << 8);
       kc += it.nch;
       ++gc;
+      itc = itn;
     }
   }
 
