@@ -1,6 +1,8 @@
 // sa_api.cu -- the C ABI (include/simplicial_attn.h): validation, kernel selection, launches.
 #include <atomic>
 #include <math.h>
+#include <stdlib.h>
+
 #include <mutex>
 #include <stdio.h>
 #include <string.h>
@@ -259,7 +261,8 @@ struct HostPipe {
   bool ok = false;
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t entry = nullptr, out = nullptr;
-  std::vector<cudaEvent_t> in, done;
+  // per chunk: forward inputs landed, dO landed, forward done (o, lse downloadable), backward done
+  std::vector<cudaEvent_t> in, in_b, fdone, done;
   std::mutex mu;
 };
 static HostPipe& host_pipe_of(int dev) {
@@ -275,11 +278,13 @@ static bool host_pipe_reserve(HostPipe& hp, int nchunks) {
             cudaEventCreateWithFlags(&hp.out, cudaEventDisableTiming) == cudaSuccess;
   }
   while (hp.ok && int(hp.in.size()) < nchunks) {
-    cudaEvent_t a, b;
-    hp.ok = cudaEventCreateWithFlags(&a, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&b, cudaEventDisableTiming) == cudaSuccess;
-    hp.in.push_back(a);
-    hp.done.push_back(b);
+    cudaEvent_t ev[4];
+    for (auto& x : ev) hp.ok = hp.ok && cudaEventCreateWithFlags(&x, cudaEventDisableTiming) == cudaSuccess;
+    if (!hp.ok) break;
+    hp.in.push_back(ev[0]);
+    hp.in_b.push_back(ev[1]);
+    hp.fdone.push_back(ev[2]);
+    hp.done.push_back(ev[3]);
   }
   return hp.ok;
 }
@@ -332,13 +337,18 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   const size_t nel = size_t(p.B) * p.N * p.H * p.D;
   // Pipeline chunks: (batch b, heads [h0, h0+hc)).  Every (b,h) slice is independent.  The
-  // first and last batch elements are split into two head halves so that the exposed first upload
-  // and last download are half a batch element; the others go whole (full-size kernel launches).
+  // first and last batch elements are split into up to 8 head groups (SA_HOSTSTEP_SPLIT; measured at
+  // c3: 8 -> 31.6 ms, 4 -> 32.2, 2 -> 32.7 per step) so that the exposed first upload and last
+  // download are small; the others go whole (full-size kernel launches).  Within a chunk the forward
+  // starts once q, k, v, k2, v2 have landed (dO uploads during it) and o, lse download during the
+  // backward.
   struct Chunk {
     int64_t b, h0, hc;
   };
   std::vector<Chunk> chunks;
-  const int64_t split = H % 4 == 0 ? 4 : (H % 2 == 0 ? 2 : 1);
+  static const int64_t max_split = getenv("SA_HOSTSTEP_SPLIT") ? atoi(getenv("SA_HOSTSTEP_SPLIT")) : 8;
+  int64_t split = 1;
+  while (split * 2 <= max_split && H % (split * 2) == 0) split *= 2;
   for (int64_t b = 0; b < B; ++b) {
     if (b == 0 || b == B - 1) {
       for (int64_t q = 0; q < split; ++q) chunks.push_back({b, q * (H / split), H / split});
@@ -377,23 +387,31 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
     // device chunk buffers: compact [N, hc, D] at the chunk's place inside batch element b's slice
     const size_t cofs = size_t((c.b * H + c.h0) * N) * row;  // elements
     auto P = [&](int t) { return base + off[t] + cofs * (t < 6 ? ein : eout); };
-    for (int t = 0; t < 6 && e == cudaSuccess; ++t) e = copy_in(P(t), hin[t], c, ein);
+    // the forward needs q, k, v, k2, v2; dO uploads while it runs
+    for (int t = 0; t < 5 && e == cudaSuccess; ++t) e = copy_in(P(t), hin[t], c, ein);
     if (e == cudaSuccess) e = cudaEventRecord(hp.in[ci], hp.h2d);
+    if (e == cudaSuccess) e = copy_in(P(5), hin[5], c, ein);
+    if (e == cudaSuccess) e = cudaEventRecord(hp.in_b[ci], hp.h2d);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.in[ci], 0);
     if (e != cudaSuccess) break;
     float* lse_c = (float*)(base + off[7]) + (c.b * H + c.h0) * N;
     s = simplicial_attn_fwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, base + off[13], off[14] - off[13], 1, c.hc,
                             N, D, w1, w2, flags, stream);
     if (s != SA_OK) return s;
+    // o and lse download while the backward runs
+    e = cudaEventRecord(hp.fdone[ci], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.fdone[ci], 0);
+    if (e == cudaSuccess) e = copy_out(h_o, P(6), c, eout);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((char*)h_lse + size_t((c.b * H + c.h0) * N) * 4, lse_c, size_t(c.hc) * N * 4,
+                          cudaMemcpyDeviceToHost, hp.d2h);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp.in_b[ci], 0);
+    if (e != cudaSuccess) break;
     s = simplicial_attn_bwd(P(0), P(1), P(2), P(3), P(4), P(6), lse_c, P(5), P(8), P(9), P(10), P(11), P(12),
                             base + off[13], off[14] - off[13], 1, c.hc, N, D, w1, w2, flags, stream);
     if (s != SA_OK) return s;
     e = cudaEventRecord(hp.done[ci], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hp.d2h, hp.done[ci], 0);
-    if (e == cudaSuccess) e = copy_out(h_o, P(6), c, eout);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync((char*)h_lse + size_t((c.b * H + c.h0) * N) * 4, lse_c, size_t(c.hc) * N * 4,
-                          cudaMemcpyDeviceToHost, hp.d2h);
     for (int t = 0; t < 5 && e == cudaSuccess; ++t) e = copy_out(hout[t], P(8 + t), c, eout);
   }
   if (e == cudaSuccess) e = cudaEventRecord(hp.out, hp.d2h);
