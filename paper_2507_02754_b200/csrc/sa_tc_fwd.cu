@@ -119,6 +119,77 @@ __device__ __forceinline__ int chunk_width(const Item& it, int c) {
   return ((it.span - kChunk * (it.nch - 1)) + 15) & ~15;
 }
 
+// Epilogue blocks for R in {2, 4, 8, 16} (compile-time R): a warp holds 32/R whole queries in aligned
+// groups of R lanes; the R-row sum of each 16-column block of v2 o U (weighted by the row's
+// e^{m_(i,k)-m_i}) by a reduce-scatter inside the group leaves 16/R columns per lane.  The next
+// block's TMEM columns are requested before this block's shuffles.
+template <int R, int D, bool STAGED>
+__device__ __forceinline__ void fwd_epi_small(const FwdArgs& a, const Item& it, uint32_t tU, const __nv_bfloat16* v2row,
+                                              bool valid, bool qlive, float crow, float invL, int lane, int i0, int g) {
+  constexpr int NF = 16 / R;  // columns per lane after the reduce-scatter
+  const int gl = lane & (R - 1);
+  int cbase = 0;
+#pragma unroll
+  for (int k = 0, st = R >> 1; st > 0; ++k, st >>= 1)
+    if (gl & st) cbase += 8 >> k;
+  const int64_t row_off = a.p.qoff(it.b, i0 + g, it.h) + cbase;
+  uint32_t u[16];
+  tmem_ld16(tU, u);
+#pragma unroll 1
+  for (int cb = 0; cb < D / 16; ++cb) {
+    tmem_ld_wait();
+    float v[16];
+    if (valid) {
+      const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint4 y = vp[t];
+        const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = bf16x2_to_f2(ys[e]);
+          v[8 * t + 2 * e] = f.x * crow * __uint_as_float(u[8 * t + 2 * e]);
+          v[8 * t + 2 * e + 1] = f.y * crow * __uint_as_float(u[8 * t + 2 * e + 1]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = 0.f;
+    }
+    if (cb + 1 < D / 16) tmem_ld16(tU + 16 * (cb + 1), u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // stages st = R/2, ..., 1 keeping n = 8, 4, 2, 1 values
+      constexpr int kR = R;
+      const int st = (kR >> 1) >> k, n = 8 >> k;
+      if (st > 0) {
+        const bool hi = gl & st;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < n) {
+            const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+          }
+        }
+      }
+    }
+    if (qlive) {
+      const int64_t off = row_off + 16 * cb;
+      if (a.out_f32) {
+#pragma unroll
+        for (int i = 0; i < NF; ++i) reinterpret_cast<float*>(a.o)[off + i] = v[i] * invL;
+      } else if constexpr (NF >= 2) {
+#pragma unroll
+        for (int i = 0; i < NF; i += 2) {
+          const __nv_bfloat162 hv = __floats2bfloat162_rn(v[i] * invL, v[i + 1] * invL);
+          *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(a.o) + off + i) = hv;
+        }
+      } else {
+        reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(v[0] * invL);
+      }
+    }
+  }
+}
+
 template <int D, bool STAGED>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FwdArgs a) {
@@ -520,65 +591,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gl = lane & (a.R - 1);  // lane within the query's group
         if (gl == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
         const float invL = qlive ? 1.f / L : 0.f;
-        const int nf = 16 / a.R;  // columns per lane after the reduce-scatter
-        int cbase = 0;
-        for (int k = 0, st = a.R >> 1; st > 0; ++k, st >>= 1)
-          if (gl & st) cbase += 8 >> k;
-#pragma unroll 1
-        for (int cb = 0; cb < D / 16; ++cb) {
-          uint32_t u[16];
-          tmem_ld16(tU + 16 * cb, u);
-          tmem_ld_wait();
-          float v[16];
-          if (valid) {
-            if (STAGED) {
-              const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
-#pragma unroll
-              for (int t = 0; t < 2; ++t) {
-                const uint4 y = vp[t];
-                const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = bf16x2_to_f2(ys[e]);
-                  v[8 * t + 2 * e] = f.x;
-                  v[8 * t + 2 * e + 1] = f.y;
-                }
-              }
-            } else {
-              load_bf16<16>(v2row + 16 * cb, v);
-            }
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] *= crow * __uint_as_float(u[e]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = 0.f;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {  // stages st = R/2, R/4, ..., 1 with n = 8, 4, 2, 1 kept values
-            const int st = (a.R >> 1) >> k, n = 8 >> k;
-            if (st > 0) {
-              const bool hi = gl & st;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (i < n) {
-                  const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
-                  v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-                }
-              }
-            }
-          }
-          if (qlive) {
-            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + cbase;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (i < nf) {
-                if (a.out_f32)
-                  reinterpret_cast<float*>(a.o)[off + i] = v[i] * invL;
-                else
-                  reinterpret_cast<__nv_bfloat16*>(a.o)[off + i] = __float2bfloat16_rn(v[i] * invL);
-              }
-            }
-          }
+        switch (a.R) {  // compile-time R: fixed shuffle strides, no runtime stage branches
+          case 2: fwd_epi_small<2, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
+          case 4: fwd_epi_small<4, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
+          case 8: fwd_epi_small<8, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
+          default: fwd_epi_small<16, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
         }
       } else if (a.R == 64 || a.R == 128) {
         // one query == two warps (R = 64: lane quarters qd, qd^1) or all four (R = 128): warp-level
