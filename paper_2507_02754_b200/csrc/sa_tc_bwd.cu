@@ -680,20 +680,18 @@ __device__ __forceinline__ void q_epilogue_rot(QSmem<D, RING, STAGED>& sm, const
   }
 }
 
-// Determinant pass over 24 columns [c0, c0+24) (eight 3-chunks), R in {32, 64}: warp m = 2 half + sub
-// of a lane quarter takes columns c0+6m..+6 (two chunks) of W (dq = s sum_k W x k2, dk2 rows
-// s q x W) and of U (dv2 rows dO o U); dq by a register reduce-scatter over the 32 lanes (six
-// values padded to eight), dk2/dv2 through the shared-memory gather in float2 pairs.  Dims past the
-// last whole chunk (D mod 3) contribute 0 (reading R5).
-// Generic-R variant of q_epilogue_pass32 (used for R in {2, 4, 8, 16}; R = 32/64 keep the
-// specialised function above).  Trilinear pass over 32 columns [c0, c0+32): the four warps of a TMEM lane quarter (= one
-// query g, 32 rows) split the columns 8 ways each: warp m = 2 half + sub takes columns c0+8m..+8
-// of both W (dq and the dk2 rows) and U (the dv2 rows).  dq is a register reduce-scatter over the
-// 32 lanes (lane groups of 4 end with one column); dk2/dv2 go through the shared-memory gather.
-template <int D, int RING, bool STAGED>
+// Small-R variant of q_epilogue_pass32 (R in {2, 4, 8, 16}, compile-time; R = 32/64 keep the
+// specialised function above).  Trilinear pass over 32 columns [c0, c0+32): warp m = 2 half + sub of
+// a TMEM lane quarter takes columns c0+8m..+8 of both W (dq and the dk2 rows) and U (the dv2 rows).
+// A warp holds 32/R whole queries in aligned groups of R lanes: dq is a reduce-scatter inside the
+// group (a lane keeps max(1, 8/R) columns; for R = 16 a final xor-1 add leaves lane pairs with the
+// same column); dk2/dv2 go through the shared-memory band gather, one thread per (key slot, 4
+// columns, k2 or v2) summing its min(R, G) rows.
+template <int D, int RING, bool STAGED, int R>
 __device__ __forceinline__ void q_epilogue_pass_small(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
-                                                  int c0, int half, int sub, int r, bool valid, const QRows& rw,
-                                                  uint32_t tW, uint32_t tU, int tidc, int sbase) {
+                                                      int c0, int half, int sub, int r, bool valid, const QRows& rw,
+                                                      uint32_t tW, uint32_t tU, int tidc, int sbase) {
+  constexpr int G = 128 / R, LR = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4, T = R < G ? R : G;
   const Problem& p = a.p;
   const float s = p.scale;
   const int ln = r & 31;
@@ -724,122 +722,72 @@ __device__ __forceinline__ void q_epilogue_pass_small(QSmem<D, RING, STAGED>& sm
   *reinterpret_cast<float4*>(&sm.eb.w.ek[r][8 * m + 4]) = make_float4(ck[4], ck[5], ck[6], ck[7]);
   *reinterpret_cast<float4*>(&sm.eb.w.ev[r][8 * m]) = make_float4(cv[0], cv[1], cv[2], cv[3]);
   *reinterpret_cast<float4*>(&sm.eb.w.ev[r][8 * m + 4]) = make_float4(cv[4], cv[5], cv[6], cv[7]);
-  if (a.R >= 32) {
-    // reduce-scatter the 8 columns over the 32 lanes: after the xor-16/8/4 stages lane L holds column
-    // (L>>4)&1 | ((L>>3)&1)<<1 | ((L>>2)&1)<<2 summed over 8 lanes; xor 2 and 1 finish the sum
+  const int gl = ln & (R - 1);
+  int cbase = 0;
 #pragma unroll
-    for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
-      const bool hi = ln & st;
+  for (int k = 0; k < 4; ++k) {  // stages st = R/2, ..., 1
+    constexpr int kR = R;
+    const int st = (kR >> 1) >> k, n = 4 >> k;
+    if (st > 0) {
+      if (n >= 1) {
+        const bool hi = gl & st;
 #pragma unroll
-      for (int i = 0; i < n; ++i) {
-        const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-      }
-    }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    const int gq = r >> a.lR;
-    const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
-    // R = 64: a query spans two lane quarters; the odd one parks its partial column sums
-    const bool lead = a.R == 32 || ((r >> 5) & 1) == 0;
-    if (!lead && (ln & 3) == 0) sm.dqx[gq][8 * m + col] = v[0];
-    if (a.R == 64) named_bar_sync(1, kQNT);
-    if (lead && (ln & 3) == 0 && gq < it.nq) {
-      const float y = a.R == 64 ? v[0] + sm.dqx[gq][8 * m + col] : v[0];
-      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + col;
-      if (a.out_f32)
-        reinterpret_cast<float*>(a.dq)[off] = y;
-      else
-        reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
-    }
-  } else {
-    // R in {2, 4, 8, 16}: the warp holds 32/R whole queries in aligned groups of R lanes; the R-row
-    // sum of the 8 columns by a reduce-scatter inside the group (lane keeps max(1, 8/R) columns;
-    // for R = 16 a final xor-1 add leaves lane pairs with the same column)
-    const int gl = ln & (a.R - 1);
-    int cbase = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int st = (a.R >> 1) >> k, n = 4 >> k;
-      if (st > 0) {
-        if (n >= 1) {
-          const bool hi = gl & st;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (i < n) {
-              const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
-              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-            }
+        for (int i = 0; i < 4; ++i) {
+          if (i < n) {
+            const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
           }
-          if (hi) cbase += n;
-        } else {
-          v[0] += __shfl_xor_sync(0xffffffffu, v[0], st);
         }
+        if (hi) cbase += n;
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], st);
       }
     }
-    const int nf = a.R >= 8 ? 1 : 8 / a.R;
-    const int gq = r >> a.lR;
-    if ((a.R < 16 || (gl & 1) == 0) && gq < it.nq) {
-      const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + cbase;
+  }
+  constexpr int NF = R >= 8 ? 1 : 8 / R;
+  const int gq = r >> LR;
+  if ((R < 16 || (gl & 1) == 0) && gq < it.nq) {
+    const int64_t off = p.qoff(it.b, it.i0 + gq, it.h) + cs + cbase;
+    if (a.out_f32) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (i < nf) {
-          if (a.out_f32)
-            reinterpret_cast<float*>(a.dq)[off + i] = v[i];
-          else
-            reinterpret_cast<__nv_bfloat16*>(a.dq)[off + i] = __float2bfloat16_rn(v[i]);
-        }
-      }
+      for (int i = 0; i < NF; ++i) reinterpret_cast<float*>(a.dq)[off + i] = v[i];
+    } else if constexpr (NF >= 2) {
+#pragma unroll
+      for (int i = 0; i < NF; i += 2)
+        *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(a.dq) + off + i) =
+            __floats2bfloat162_rn(v[i], v[i + 1]);
+    } else {
+      reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
     }
   }
   named_bar_sync(1, kQNT);
   const int P0 = p.np + it.i0;
-  const int nsl = a.R + it.nq - 1;
-  // key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g); thread -> (sl, 4 columns)
-  for (int idx = tidc; idx < nsl * 8; idx += kQNT) {
-    const int sl = idx >> 3, d = 4 * (idx & 7);
-    const int kp = P0 - a.R + 1 + sl;
-    const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
-    float4 sk = make_float4(0.f, 0.f, 0.f, 0.f), sv4 = sk;
-    if (a.G <= 4) {  // R >= 32: at most 4 terms, loads first (unrolled)
-      float4 tk[4], tv[4];
+  const int nsl = R + it.nq - 1;
+  // key row kpos = P0 - R + 1 + sl receives rows (g, kk = sl - g); thread -> (sl, 4 columns, k2|v2)
+  for (int idx = tidc; idx < nsl * 16; idx += kQNT) {
+    const int which = idx & 1, sl = idx >> 4, d = 4 * ((idx >> 1) & 7);
+    const int kp = P0 - R + 1 + sl;
+    const int glo = max(0, sl - R + 1), ghi = min(it.nq - 1, sl);
+    const float(*src)[36] = which ? sm.eb.w.ev : sm.eb.w.ek;
+    float4 t[T];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int gg = glo + u;
-        const int row = (gg << a.lR) + (sl - gg);
-        tk[u] = tv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gg <= ghi) {
-          tk[u] = *reinterpret_cast<const float4*>(&sm.eb.w.ek[row][d]);
-          tv[u] = *reinterpret_cast<const float4*>(&sm.eb.w.ev[row][d]);
-        }
-      }
-      sk.x = (tk[0].x + tk[1].x) + (tk[2].x + tk[3].x);
-      sk.y = (tk[0].y + tk[1].y) + (tk[2].y + tk[3].y);
-      sk.z = (tk[0].z + tk[1].z) + (tk[2].z + tk[3].z);
-      sk.w = (tk[0].w + tk[1].w) + (tk[2].w + tk[3].w);
-      sv4.x = (tv[0].x + tv[1].x) + (tv[2].x + tv[3].x);
-      sv4.y = (tv[0].y + tv[1].y) + (tv[2].y + tv[3].y);
-      sv4.z = (tv[0].z + tv[1].z) + (tv[2].z + tv[3].z);
-      sv4.w = (tv[0].w + tv[1].w) + (tv[2].w + tv[3].w);
-    } else {
-      for (int gg = glo; gg <= ghi; ++gg) {  // min(R, G) terms
-        const int row = (gg << a.lR) + (sl - gg);
-        const float4 tk = *reinterpret_cast<const float4*>(&sm.eb.w.ek[row][d]);
-        const float4 tv = *reinterpret_cast<const float4*>(&sm.eb.w.ev[row][d]);
-        sk.x += tk.x, sk.y += tk.y, sk.z += tk.z, sk.w += tk.w;
-        sv4.x += tv.x, sv4.y += tv.y, sv4.z += tv.z, sv4.w += tv.w;
-      }
+    for (int u = 0; u < T; ++u) {
+      const int gg = glo + u;
+      t[u] = gg <= ghi ? *reinterpret_cast<const float4*>(&src[(gg << LR) + (sl - gg)][d])
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+#pragma unroll
+    for (int w = 1; w < T; w <<= 1)
+#pragma unroll
+      for (int u = 0; u + w < T; u += 2 * w)
+        t[u] = make_float4(t[u].x + t[u + w].x, t[u].y + t[u + w].y, t[u].z + t[u + w].z, t[u].w + t[u + w].w);
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
     if (kp >= 0) {
-      float4* ak = reinterpret_cast<float4*>(&q_acc(sm, a, 0)[slot][c0 + d]);
-      float4* av = reinterpret_cast<float4*>(&q_acc(sm, a, 1)[slot][c0 + d]);
-      float4 xk = *ak, xv = *av;
-      xk.x += sk.x, xk.y += sk.y, xk.z += sk.z, xk.w += sk.w;
-      xv.x += sv4.x, xv.y += sv4.y, xv.z += sv4.z, xv.w += sv4.w;
-      *ak = xk;
-      *av = xv;
+      float4* acc = reinterpret_cast<float4*>(&q_acc(sm, a, which)[slot][c0 + d]);
+      float4 x = *acc;
+      x.x += t[0].x, x.y += t[0].y, x.z += t[0].z, x.w += t[0].w;
+      *acc = x;
     }
   }
   named_bar_sync(1, kQNT);
@@ -1623,10 +1571,15 @@ __global__ void __launch_bounds__(kQThreads, 1)
           SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | (c0 / 32));
         }
       } else if (a.R >= 2 && a.R < 32) {
-#pragma unroll 1
         const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
+#pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
-          q_epilogue_pass_small<D, RING, STAGED>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase);
+          switch (a.R) {
+            case 2: q_epilogue_pass_small<D, RING, STAGED, 2>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase); break;
+            case 4: q_epilogue_pass_small<D, RING, STAGED, 4>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase); break;
+            case 8: q_epilogue_pass_small<D, RING, STAGED, 8>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase); break;
+            default: q_epilogue_pass_small<D, RING, STAGED, 16>(sm, a, it, c0, half, sub, r, valid, rw, tW, tU, tid256, sbase); break;
+          }
           SA_TRACE_AT(tr, treg, trn, (item - it_begin) << 16 | 6 << 8 | (c0 / 32));
         }
       } else {

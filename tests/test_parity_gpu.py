@@ -86,6 +86,8 @@ def test_fp32_shapes(B, N, H, D, w1, w2, det):
     (1, 200, 2, 128, 32, 8),     # R = 8 (G = 16): the memory-bound small-window point of §8(d)
     (1, 96, 1, 64, 20, 4),       # R = 4
     (1, 70, 1, 128, 10, 2),      # R = 2 (G = 64)
+    (1, 180, 2, 128, 24, 16),    # R = 16, D = 128 (G = 8: the band gather has G < R terms)
+    (1, 150, 1, 128, 12, 5),     # w2 = 5 -> R = 8 with masked rows
     (1, 400, 1, 128, 128, 128),  # R = 128 (G = 1): Table 1's (128, 128) row, dK'/dV' ring in global memory
     (1, 300, 2, 64, 200, 128),   # R = 128, D = 64, ragged
     (1, 260, 1, 128, 128, 300),  # w2 > w1 = 128: swapped, R = 128
