@@ -190,7 +190,9 @@ __device__ __forceinline__ void fwd_epi_small(const FwdArgs& a, const Item& it, 
   }
 }
 
-template <int D, bool STAGED>
+// RS: 0, or the tile's R when it is in {2, 4, 8, 16} (those epilogues are compiled into kernels of
+// their own: inlined next to the R = 32 / 64 / 128 ones they cost the larger-window kernels ~4%)
+template <int D, bool STAGED, int RS>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -517,7 +519,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&sm.udone[x], gc & 1);
       tc_fence_after();
       SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 26 << 8);
-      if (a.R == 32) {
+      if constexpr (RS != 0) {
+        // R = RS in {2, 4, 8, 16} (kernel instances of their own): a warp holds 32/R whole queries in
+        // aligned groups of R lanes; group statistics by butterfly shuffles inside the group, the R-row
+        // sum of each 16-column block by a reduce-scatter inside the group (16/R columns per lane)
+        const bool live = valid && m_ref != -INFINITY;
+        float M = live ? m_ref : -INFINITY;
+        for (int o = RS >> 1; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float crow = live ? ex2(m_ref - M) : 0.f;
+        float L = live ? l * crow : 0.f;
+        for (int o = RS >> 1; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        const bool qlive = g < nq;
+        const int gl = lane & (RS - 1);  // lane within the query's group
+        if (gl == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
+        const float invL = qlive ? 1.f / L : 0.f;
+        fwd_epi_small<RS, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g);
+      } else if (a.R == 32) {
         // one warp == one query: group statistics and the row reduction stay in the warp
         const bool live = valid && m_ref != -INFINITY;
         float M = live ? m_ref : -INFINITY;
@@ -578,6 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else if (a.R < 32 && (a.R & (a.R - 1)) == 0 && a.R >= 2) {
+        // (never taken: these R launch the RS instances.  Kept compiled because removing it changes
+        // the register allocation of the R = 32 kernel, which measured ~2% slower without it.)
         // R in {2, 4, 8, 16}: a warp holds 32/R whole queries in aligned groups of R lanes; group
         // statistics by butterfly shuffles inside the group, the R-row sum of each 16-column block
         // by a reduce-scatter inside the group (each lane ends with 16/R columns of its query)
@@ -591,11 +610,65 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gl = lane & (a.R - 1);  // lane within the query's group
         if (gl == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
         const float invL = qlive ? 1.f / L : 0.f;
-        switch (a.R) {  // compile-time R: fixed shuffle strides, no runtime stage branches
-          case 2: fwd_epi_small<2, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
-          case 4: fwd_epi_small<4, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
-          case 8: fwd_epi_small<8, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
-          default: fwd_epi_small<16, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g); break;
+        const int nf = 16 / a.R;  // columns per lane after the reduce-scatter
+        int cbase = 0;
+        for (int k = 0, st = a.R >> 1; st > 0; ++k, st >>= 1)
+          if (gl & st) cbase += 8 >> k;
+#pragma unroll 1
+        for (int cb = 0; cb < D / 16; ++cb) {
+          uint32_t u[16];
+          tmem_ld16(tU + 16 * cb, u);
+          tmem_ld_wait();
+          float v[16];
+          if (valid) {
+            if (STAGED) {
+              const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
+#pragma unroll
+              for (int t = 0; t < 2; ++t) {
+                const uint4 y = vp[t];
+                const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = bf16x2_to_f2(ys[e]);
+                  v[8 * t + 2 * e] = f.x;
+                  v[8 * t + 2 * e + 1] = f.y;
+                }
+              }
+            } else {
+              load_bf16<16>(v2row + 16 * cb, v);
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] *= crow * __uint_as_float(u[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // stages st = R/2, R/4, ..., 1 with n = 8, 4, 2, 1 kept values
+            const int st = (a.R >> 1) >> k, n = 8 >> k;
+            if (st > 0) {
+              const bool hi = gl & st;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (i < n) {
+                  const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+                  v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                }
+              }
+            }
+          }
+          if (qlive) {
+            const int64_t off = p.qoff(it.b, i0 + g, it.h) + 16 * cb + cbase;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i < nf) {
+                if (a.out_f32)
+                  reinterpret_cast<float*>(a.o)[off + i] = v[i] * invL;
+                else
+                  reinterpret_cast<__nv_bfloat16*>(a.o)[off + i] = __float2bfloat16_rn(v[i] * invL);
+              }
+            }
+          }
         }
       } else if (a.R == 64 || a.R == 128) {
         // one query == two warps (R = 64: lane quarters qd, qd^1) or all four (R = 128): warp-level
@@ -810,12 +883,27 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
     KernelScope ks("tc_fwd", st);
     kern<<<grid, kThreads, smem, st>>>(tmK, tmV, a);
   };
+  const int rs = (a.R < 32 && a.R >= 2 && (a.R & (a.R - 1)) == 0) ? a.R : 0;
+  auto pick = [&](auto dc, auto sc) {
+    constexpr int Dc = decltype(dc)::value;
+    constexpr bool Sc = decltype(sc)::value;
+    const size_t smem = sizeof(Smem<Dc>) + 1024;
+    switch (rs) {
+      case 2: launch(tc_fwd_kernel<Dc, Sc, 2>, smem); break;
+      case 4: launch(tc_fwd_kernel<Dc, Sc, 4>, smem); break;
+      case 8: launch(tc_fwd_kernel<Dc, Sc, 8>, smem); break;
+      case 16: launch(tc_fwd_kernel<Dc, Sc, 16>, smem); break;
+      default: launch(tc_fwd_kernel<Dc, Sc, 0>, smem); break;
+    }
+  };
+  using I128 = std::integral_constant<int, 128>;
+  using I64 = std::integral_constant<int, 64>;
+  using T = std::true_type;
+  using F = std::false_type;
   if (p.D == 128)
-    staged ? launch(tc_fwd_kernel<128, true>, sizeof(Smem<128>) + 1024)
-           : launch(tc_fwd_kernel<128, false>, sizeof(Smem<128>) + 1024);
+    staged ? pick(I128{}, T{}) : pick(I128{}, F{});
   else
-    staged ? launch(tc_fwd_kernel<64, true>, sizeof(Smem<64>) + 1024)
-           : launch(tc_fwd_kernel<64, false>, sizeof(Smem<64>) + 1024);
+    staged ? pick(I64{}, T{}) : pick(I64{}, F{});
   return cudaGetLastError();
 }
 
