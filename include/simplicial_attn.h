@@ -81,8 +81,10 @@ enum {
 enum { SA_PATH_SIMT = 1, SA_PATH_TCGEN05 = 2 };
 
 /* Bytes of device workspace the forward needs (the tensor-core path keeps fp16 copies of q, k, v
- * and the folded key there); 0 for the fp32 path.  The _prefixed form sizes it for n_prefix halo
- * rows.  Returns 0 for invalid arguments as well. */
+ * and the folded key there; a folded window over 64 rows, or over 32 with w1 <= 256, also keeps
+ * the fp32 partial outputs of its <= 32-row sub-windows: the window split of DESIGN.md); 0 for
+ * the fp32 path.  The _prefixed form sizes it for n_prefix halo rows.  Returns 0 for invalid
+ * arguments as well. */
 size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
                                            int64_t w2, uint32_t flags);
 size_t simplicial_attn_fwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D,
@@ -106,7 +108,9 @@ sa_status simplicial_attn_fwd_prefixed(const void* q, const void* k, const void*
                                        uint32_t flags, void* stream);
 
 /* Bytes of device workspace the backward needs (delta_i [B,H,N] fp32, fp16 copies of the
- * key-side operands, band partials).  The _prefixed form sizes it for n_prefix halo rows. */
+ * key-side operands, band partials; for a folded window over 32 rows also one fp32 set of the five
+ * gradients per <= 32-row sub-window, summed into the outputs: the window split of DESIGN.md).
+ * The _prefixed form sizes it for n_prefix halo rows. */
 size_t simplicial_attn_bwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
                                            int64_t w2, uint32_t flags);
 size_t simplicial_attn_bwd_workspace_bytes_prefixed(int64_t B, int64_t H, int64_t N, int64_t D,

@@ -100,6 +100,7 @@ static sa_status make_problem(int64_t B, int64_t H, int64_t N, int64_t D, int64_
   p->w1 = int(w1); p->w2 = int(w2); p->np = int(n_prefix);
   p->Hk = int(H);
   p->hk_shift = 0;
+  p->k2lo = 0;
   p->det = (flags & SA_VARIANT_DET) != 0;
   p->scale = float(1.0 / sqrt(double(D)));
   return SA_OK;

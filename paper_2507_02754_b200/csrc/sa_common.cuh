@@ -16,6 +16,10 @@ struct Problem {
   int hk_shift;                // log2(H / Hk) when that ratio is a power of two (the usual case), else -1
   float scale;                 // signed logit scale (negated when the DET operands are swapped)
   bool det;
+  // Lowest valid K' row index (0 normally).  The backward / forward of a window w2 > 32 runs as
+  // w2/32 sub-problems of window 32 whose K' rows are shifted by d: the
+  // kernels see K' through a pointer offset by -d rows, so virtual rows < k2lo = d do not exist.
+  int k2lo;
   __host__ __device__ int NK() const { return np + N; }
   __host__ __device__ int hk(int h) const { return hk_shift >= 0 ? h >> hk_shift : h / (H / Hk); }
   // element offsets of row (b, pos, h) in query-side tensors and in per-query-head key-side

@@ -344,7 +344,7 @@ __device__ __forceinline__ void q_epilogue_pass(QSmem<D, RING, STAGED>& sm, cons
   for (int idx = tid256; idx < nsl * PW; idx += kQNT) {
     const int sl = idx / PW, d = idx % PW;
     const int kp = P0 - a.R + 1 + sl;
-    if (kp < 0) continue;
+    if (kp < a.p.k2lo) continue;
     float xk = 0.f, xv = 0.f;
     const int glo = max(0, sl - a.R + 1), ghi = min(it.nq - 1, sl);
     for (int g0 = glo; g0 <= ghi; g0 += 4) {
@@ -453,7 +453,7 @@ __device__ __forceinline__ void q_epilogue_pass32(QSmem<D, RING, STAGED>& sm, co
     }
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
-    if (kp >= 0) {
+    if (kp >= a.p.k2lo) {
       float4* ak = reinterpret_cast<float4*>(&q_acc(sm, a, 0)[slot][c0 + d]);
       float4* av = reinterpret_cast<float4*>(&q_acc(sm, a, 1)[slot][c0 + d]);
       float4 xk = *ak, xv = *av;
@@ -783,7 +783,7 @@ __device__ __forceinline__ void q_epilogue_pass_small(QSmem<D, RING, STAGED>& sm
         t[u] = make_float4(t[u].x + t[u + w].x, t[u].y + t[u + w].y, t[u].z + t[u + w].z, t[u].w + t[u + w].w);
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
-    if (kp >= 0) {
+    if (kp >= a.p.k2lo) {
       float4* acc = reinterpret_cast<float4*>(&q_acc(sm, a, which)[slot][c0 + d]);
       float4 x = *acc;
       x.x += t[0].x, x.y += t[0].y, x.z += t[0].z, x.w += t[0].w;
@@ -903,7 +903,7 @@ __device__ __forceinline__ void q_epilogue_pass_det(QSmem<D, RING, STAGED>& sm, 
     }
     int slot = sbase + sl;
     if (slot >= a.ring) slot -= a.ring;
-    if (kp >= 0) {
+    if (kp >= a.p.k2lo) {
       float2* ak = reinterpret_cast<float2*>(&q_acc(sm, a, 0)[slot][c0 + d]);
       float2* av = reinterpret_cast<float2*>(&q_acc(sm, a, 1)[slot][c0 + d]);
       float2 yk = *ak, yv = *av;
@@ -1222,7 +1222,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           } else {
             const int rr = row - 2 * a.G;
             const int kp = P0 - a.R + 1 + (rr < nk ? rr : rr - nk);
-            if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.kvoff(it.b, kp, it.hk);
+            if (kp >= p.k2lo && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.kvoff(it.b, kp, it.hk);
           }
           if (src) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 64 * ln128));
         }
@@ -1247,7 +1247,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
             const int rr = row - 2 * a.G;
             const bool isv = rr >= nkn;
             const int kp = klo + (isv ? rr - nkn : rr);
-            if (kp >= 0 && kp < p.NK()) src = (isv ? a.v2 : a.k2) + p.kvoff(it.b, kp, it.hk);
+            if (kp >= p.k2lo && kp < p.NK()) src = (isv ? a.v2 : a.k2) + p.kvoff(it.b, kp, it.hk);
             dst = isv ? &sm.rv2[rh][kp >= 0 ? kp % Sm::kKR : 0][0] : &sm.rk2[rh][kp >= 0 ? kp % Sm::kKR : 0][0];
           }
           if (src) cp_async16(dst + 8 * c8, src + 8 * c8);
@@ -1276,7 +1276,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         } else {
           const int rr = row - 2 * a.G;
           const int kp = P0 - a.R + 1 + (rr < nk ? rr : rr - nk);
-          if (kp >= 0 && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.kvoff(it.b, kp, it.hk);
+          if (kp >= p.k2lo && kp < p.NK()) src = (rr < nk ? a.k2 : a.v2) + p.kvoff(it.b, kp, it.hk);
         }
         if (src) cp_async16(&sm.stg[buf][row][8 * c8], src + 8 * c8);
       }
@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int fP0 = p.np + fi.i0;
       const int g = r >> a.lR, kk = r & (a.R - 1);
       const int fkpos = fP0 + g - a.R + 1 + kk;
-      const bool fvalid = r < a.G * a.R && g < fi.nq && fkpos >= 0;
+      const bool fvalid = r < a.G * a.R && g < fi.nq && fkpos >= p.k2lo;
       QRows fr{};
       if (fvalid) {
         const int nk = a.R + a.G - 1;
@@ -1419,7 +1419,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool row_in = r < a.G * a.R && g < it.nq;
       const int pos = P0 + g;
       const int kpos = pos - a.R + 1 + kk;
-      const bool valid = row_in && kpos >= 0 && kk >= a.R - a.Rt;
+      const bool valid = row_in && kpos >= p.k2lo && kk >= a.R - a.Rt;
       float lse_l2 = 0.f, dl = 0.f;
       QRows rw{};
       if (row_in) {
@@ -1597,7 +1597,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int fbase = a.fd_ring.mod(flush_lo + a.ring);
       for (int idx = tid256; idx < nrows * D; idx += kQNT) {
         const int kp = flush_lo + idx / D, d = idx % D;
-        if (kp < 0 || kp >= p.NK()) continue;
+        if (kp < p.k2lo || kp >= p.NK()) continue;
         int slot = fbase + idx / D;
         if (slot >= a.ring) slot -= a.ring;
         const float vk = q_acc(sm, a, 0)[slot][d], vv = q_acc(sm, a, 1)[slot][d];
@@ -1656,21 +1656,21 @@ __global__ void __launch_bounds__(256) fold_kernel(BwdQArgs a, int grid_q) {
       for (int idx = threadIdx.x; idx < Rm1 * D; idx += blockDim.x) {
         const int rr = idx / D, d = idx % D;
         const int kp = PS - a.R + 1 + rr;
-        if (kp < 0) continue;
+        if (kp < p.k2lo) continue;
         const int64_t off = p.koff(b, kp, h) + d;
         st_f(reinterpret_cast<TOut*>(a.dk2) + off, left[idx] + right[idx]);
         st_f(reinterpret_cast<TOut*>(a.dv2) + off, left[size_t(Rm1) * D + idx] + right[size_t(Rm1) * D + idx]);
       }
     }
   }
-  // prefix rows [0, np - R + 1) are outside every query's window: zero
-  const int nz = p.np - a.R + 1;
+  // prefix rows [k2lo, np - R + 1) are outside every query's window: zero
+  const int nz = p.np - a.R + 1 - p.k2lo;
   if (nz > 0) {
     const int64_t total = int64_t(p.B) * p.H * nz * D;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
       const int d = e % D;
       const int64_t t = e / D;
-      const int kp = t % nz, bh = t / nz, b = bh / p.H, h = bh % p.H;
+      const int kp = p.k2lo + int(t % nz), bh = t / nz, b = bh / p.H, h = bh % p.H;
       const int64_t off = p.koff(b, kp, h) + d;
       st_f(reinterpret_cast<TOut*>(a.dk2) + off, 0.f);
       st_f(reinterpret_cast<TOut*>(a.dv2) + off, 0.f);
@@ -1790,7 +1790,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         for (int task = ft; task < nk * kC8; task += kNF) {
           const int off = task / kC8, c8 = task % kC8;  // kC8 is a compile-time power of two
           const int kp = klo + off;
-          if (kp < 0 || kp >= p.NK()) continue;
+          if (kp < p.k2lo || kp >= p.NK()) continue;
           int slot = slo + off;
           if (slot >= a.ring) slot -= a.ring;
           const __half* src = (which ? a.v2 : a.k2) + p.kvoff(b, kp, hkv) + 8 * c8;
@@ -1844,7 +1844,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int g = r >> a.lR, kk = r & (a.R - 1);
         const int i = q0 + g;
         const int kpos = kbase + g + kk;
-        const bool valid = r < a.G * a.R && i < qb && kpos >= 0 && kk >= a.R - a.Rt;
+        const bool valid = r < a.G * a.R && i < qb && kpos >= p.k2lo && kk >= a.R - a.Rt;
         float2 ri = make_float2(INFINITY, 0.f);
         if (valid) {
           if (STAGED) {
@@ -1880,7 +1880,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         if (slot >= a.ring) slot -= a.ring;
 #pragma unroll
         for (int u = 0; u < kRB8; ++u) {
-          const bool ok = qok && kbase + g + kk0 + u >= 0;
+          const bool ok = qok && kbase + g + kk0 + u >= p.k2lo;
           int su = slot + u;
           if (su >= a.ring) su -= a.ring;
           yk[u] = wv[u] = make_uint4(0u, 0u, 0u, 0u);
@@ -1912,7 +1912,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             const int r = 2 * rp;  // rows r, r+1 (R even: same query)
             const int g2 = r >> a.lR, kk2 = r & (a.R - 1);
             const bool qok = r < a.G * a.R && q0 + g2 < qb;
-            const bool ok0 = qok && kbase + g2 + kk2 >= 0, ok1 = qok && kbase + g2 + kk2 + 1 >= 0;
+            const bool ok0 = qok && kbase + g2 + kk2 >= p.k2lo, ok1 = qok && kbase + g2 + kk2 + 1 >= p.k2lo;
             uint32_t pk0[12], pk1[12];
 #pragma unroll
             for (int e = 0; e < 12; ++e) pk0[e] = pk1[e] = 0u;
@@ -2009,7 +2009,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           int slot = sbase + kr;
           if (slot >= a.ring) slot -= a.ring;
           uint4 yk = make_uint4(0u, 0u, 0u, 0u), wv = yk;
-          if (kpos >= 0) {
+          if (kpos >= p.k2lo) {
             yk = *reinterpret_cast<const uint4*>(&sm.rk2[slot][8 * c8]);
             wv = *reinterpret_cast<const uint4*>(&sm.rv2[slot][8 * c8]);
           }
@@ -2017,7 +2017,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           for (int g = 0; g < 4; ++g) {
             const int kk = kr - g;
             if (g >= a.G || kk < 0 || kk >= a.R) continue;
-            const bool ok = q0 + g < qb && kpos >= 0;
+            const bool ok = q0 + g < qb && kpos >= p.k2lo;
             uint4 oa = make_uint4(0u, 0u, 0u, 0u), od = oa;
             if (ok) {
               oa = make_uint4(hmul2_u32(xq[g].x, yk.x), hmul2_u32(xq[g].y, yk.y), hmul2_u32(xq[g].z, yk.z),
@@ -2054,7 +2054,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
             const int g = r >> a.lR, kk = r & (a.R - 1);
             const int i = q0 + g;
             const int kpos = kbase + g + kk;
-            ok[u] = r < a.G * a.R && i < qb && kpos >= 0;
+            ok[u] = r < a.G * a.R && i < qb && kpos >= p.k2lo;
             int slot = sbase + g + kk;
             if (slot >= a.ring) slot -= a.ring;
             if (ok[u]) {
@@ -2093,7 +2093,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
         const int g = r >> a.lR, kk = r & (a.R - 1);
         const int i = q0 + g;
         const int kpos = kbase + g + kk;
-        const bool valid = r < a.G * a.R && i < qb && kpos >= 0 && kk >= a.R - a.Rt;
+        const bool valid = r < a.G * a.R && i < qb && kpos >= p.k2lo && kk >= a.R - a.Rt;
         int slot = sbase + g + kk;
         if (slot >= a.ring) slot -= a.ring;
         const __half* qrow = STAGED ? &sm.sq[buf][g][0] : a.q + p.qoff(b, i, h);
@@ -2294,7 +2294,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const bool all_in = (jw0 + 31 <= P0) && (jw0 > P0 + a.G - 1 - p.w1);
       // fast path: the quarter's 32 columns belong to one query (R >= 32), no column is masked and no
       // row precedes the sequence start -> one (lse, delta) pair, packed math
-      const bool fast = all_in && a.R >= 32 && a.Rt == a.R && P0 - a.R + 1 >= 0;
+      const bool fast = all_in && a.R >= 32 && a.Rt == a.R && P0 - a.R + 1 >= p.k2lo;
       uint32_t su[32], du[32];
       tmem_ld32(tS, su);
       tmem_ld32(tdP, du);
@@ -2412,6 +2412,9 @@ cudaError_t tc_bwd_q2_launch(const Problem& p, bool out_f32, const CUtensorMap& 
                              const float* delta, void* dq, void* dk2, void* dv2, float* band, int R, int G,
                              cudaStream_t st);
 
+cudaError_t split_sum(const float* part, int64_t part_stride, int nsplit, int shift_step, void* out, bool out_f32,
+                      int64_t n, int rows, int64_t row_stride, cudaStream_t st);
+
 cudaError_t simt_bwd_dk_only(const Problem& p, bool out_f32, const void* q, const void* k, const void* v,
                              const void* k2, const void* v2, const void* dO, const float* lse, const float* delta,
                              void* dk, void* dv, cudaStream_t st);
@@ -2452,17 +2455,43 @@ static int q_grid(const Problem& p, int R, int G, int* per_cta, int* items_out) 
   return grid;
 }
 
+// Window split (sa_split.cu): a folded window w2 > 32 runs as sub-problems of <= 32 rows, sub-problem
+// b covering K' offsets [32 b, 32 b + w_b) back from the query.  SA_NO_WSPLIT=1 keeps the single
+// R = 64 / 128 tiling (A/B experiments).
+static int split_count(const Problem& p) {
+  static const bool off = getenv("SA_NO_WSPLIT") && atoi(getenv("SA_NO_WSPLIT")) != 0;
+  if (off || p.w2 <= 32) return 1;
+  return (p.w2 + 31) / 32;
+}
+static Problem split_problem(const Problem& p, int b) {
+  Problem s = p;
+  s.k2lo = 32 * b;
+  s.w2 = std::min(32, p.w2 - 32 * b);
+  return s;
+}
+
+// scratch of one (sub-)problem's bwd_q / bwd_kv launches: band workspace and the R = 128 det ring slab
+static size_t bwd_core_bytes(const Problem& p) {
+  const int R = tile_rows(p.w2), G = 128 / R;
+  return a256(sizeof(float) * size_t(q_grid_n(p, R, G)) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D) +
+         (R + G > kRingMax && p.det ? a256(sizeof(float) * size_t(q_grid_n(p, R, G)) * 2 * (R + G) * p.D) : 0);
+}
+
 size_t tc_bwd_workspace_bytes(const Problem& p0) {
   Problem p = p0;
   if (swapped(p)) std::swap(p.w1, p.w2);
-  const int R = tile_rows(p.w2), G = 128 / R;
-  int pc, items;
-  const int grid = q_grid(p, R, G, &pc, &items);
   const size_t n = p.nkey(), nq = size_t(p.B) * p.N * p.H * p.D;
-  return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 4 * a256(n * 2) + 2 * a256(nq * 2) +
-         a256(sizeof(float) * size_t(grid) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D) +
-         (R + G > kRingMax && p.det ? a256(sizeof(float) * size_t(grid) * 2 * (R + G) * p.D) : 0);
+  const size_t nkh = size_t(p.B) * p.NK() * p.H * p.D;  // per-query-head key-side gradient
+  size_t core = 0, parts = 0;
+  const int ns = split_count(p);
+  for (int b = 0; b < ns; ++b) core = std::max(core, bwd_core_bytes(ns > 1 ? split_problem(p, b) : p));
+  if (ns > 1) parts = size_t(ns) * (a256(4 * nq) + 4 * a256(4 * nkh));
+  return a256(sizeof(float) * size_t(p.B) * p.H * p.N) + 4 * a256(n * 2) + 2 * a256(nq * 2) + core + parts;
 }
+
+static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, const char* vf, const char* k2f,
+                            const char* v2f, const char* qf, const char* dof, const float* lse, const float* delta,
+                            void* dq, void* dk, void* dv, void* dk2, void* dv2, char* w, cudaStream_t st);
 
 cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const void* k, const void* v, const void* k2,
                         const void* v2, const void* o, const float* lse, const void* dO, void* dq, void* dk, void* dv,
@@ -2477,7 +2506,6 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
     if (p.det) p.scale = -p.scale;
   }
   if (ws_bytes < tc_bwd_workspace_bytes(p0)) return cudaErrorInvalidValue;
-  const int Rt = p.w2, R = tile_rows(Rt), G = 128 / R;
   const size_t n = p.nkey();
   char* w = (char*)ws;
   float* delta = (float*)w;
@@ -2495,9 +2523,6 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   w += a256(nq * 2);
   char* dof = w;
   w += a256(nq * 2);
-  float* band = (float*)w;
-  w += a256(sizeof(float) * size_t(q_grid_n(p, R, G)) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
-  float* gring = R + G > kRingMax && p.det ? (float*)w : nullptr;  // R = 128 determinant only
 
   // delta
   {
@@ -2513,6 +2538,52 @@ cudaError_t tc_backward(const Problem& p0, bool out_f32, const void* q, const vo
   if (e == cudaSuccess) e = convert_pair_f16(k2, k2f, v2, v2f, int64_t(n), num_sms(), st);
   if (e == cudaSuccess) e = convert_pair_f16(q, qf, dO, dof, int64_t(nq), num_sms(), st);
   if (e != cudaSuccess) return e;
+
+  const int ns = split_count(p);
+  if (ns == 1) return bwd_core(p, out_f32, kf, vf, k2f, v2f, qf, dof, lse, delta, dq, dk, dv, dk2, dv2, w, st);
+
+  // window split: sub-problem b writes fp32 partials (its dK'/dV' through pointers shifted by -d_b rows)
+  size_t core = 0;
+  for (int b = 0; b < ns; ++b) core = std::max(core, bwd_core_bytes(split_problem(p, b)));
+  char* parts = w + core;
+  const size_t nkh = size_t(p.B) * p.NK() * p.H * p.D;
+  const size_t set = a256(4 * nq) + 4 * a256(4 * nkh);  // one sub-problem's partials, in floats below
+  const int64_t kstep = int64_t(p.Hk) * p.D, gstep = int64_t(p.H) * p.D;  // one key row: input / gradient
+  for (int b = 0; b < ns && e == cudaSuccess; ++b) {
+    const Problem sp = split_problem(p, b);
+    char* s = parts + size_t(b) * set;
+    float* pdq = (float*)s;
+    float* pdk = (float*)(s + a256(4 * nq));
+    float* pdv = pdk + a256(4 * nkh) / 4;
+    float* pdk2 = pdv + a256(4 * nkh) / 4;
+    float* pdv2 = pdk2 + a256(4 * nkh) / 4;
+    const int64_t d = sp.k2lo;
+    e = bwd_core(sp, true, kf, vf, (const char*)((const __half*)k2f - d * kstep),
+                 (const char*)((const __half*)v2f - d * kstep), qf, dof, lse, delta, pdq, pdk, pdv, pdk2 - d * gstep,
+                 pdv2 - d * gstep, w, st);
+  }
+  // sums: dq, dk, dv over every partial; dk2, dv2 over the partials that cover the row
+  const int64_t sstride = int64_t(set / 4);
+  float* p0f = (float*)parts;
+  const int64_t o_k = int64_t(a256(4 * nq) / 4), o_s = int64_t(a256(4 * nkh) / 4);
+  if (e == cudaSuccess) e = split_sum(p0f, sstride, ns, 0, dq, out_f32, int64_t(nq), p.N, gstep, st);
+  if (e == cudaSuccess) e = split_sum(p0f + o_k, sstride, ns, 0, dk, out_f32, int64_t(nkh), p.NK(), gstep, st);
+  if (e == cudaSuccess) e = split_sum(p0f + o_k + o_s, sstride, ns, 0, dv, out_f32, int64_t(nkh), p.NK(), gstep, st);
+  if (e == cudaSuccess)
+    e = split_sum(p0f + o_k + 2 * o_s, sstride, ns, 32, dk2, out_f32, int64_t(nkh), p.NK(), gstep, st);
+  if (e == cudaSuccess)
+    e = split_sum(p0f + o_k + 3 * o_s, sstride, ns, 32, dv2, out_f32, int64_t(nkh), p.NK(), gstep, st);
+  return e;
+}
+
+static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, const char* vf, const char* k2f,
+                            const char* v2f, const char* qf, const char* dof, const float* lse, const float* delta,
+                            void* dq, void* dk, void* dv, void* dk2, void* dv2, char* w, cudaStream_t st) {
+  const int Rt = p.w2, R = tile_rows(Rt), G = 128 / R;
+  float* band = (float*)w;
+  w += a256(sizeof(float) * size_t(q_grid_n(p, R, G)) * 4 * (R - 1 > 0 ? R - 1 : 1) * p.D);
+  float* gring = R + G > kRingMax && p.det ? (float*)w : nullptr;  // R = 128 determinant only
+  cudaError_t e = cudaSuccess;
 
   // bwd_q: dq, dk2, dv2
   {

@@ -12,6 +12,7 @@
 // operands with fp32 accumulation (K/V converted from bf16 exactly by a pre-pass).  Two tiles per
 // CTA ping-pong (FA4 pattern) so softmax and tensor work overlap; see the kernel comment below.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <utility>
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           const int rr = row - 2 * a.G;
           const int kp = kb + (rr < nk2 ? rr : rr - nk2);
-          if (kp >= 0 && kp < p.NK())
+          if (kp >= p.k2lo && kp < p.NK())
             src = rr < nk2 ? (const void*)(a.k2 + p.kvoff(it.b, kp, it.hk) + 8 * c8)
                            : (const void*)(a.v2 + p.kvoff(it.b, kp, it.hk) + 8 * c8);
         }
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int fi0 = (2 * fit.pair + x) * a.G;
       const int fnq = max(0, min(a.G, p.N - fi0));
       const int fkpos = p.np + fi0 + g - a.R + 1 + kk;
-      const bool fvalid = r < a.G * a.R && g < fnq && fkpos >= 0;
+      const bool fvalid = r < a.G * a.R && g < fnq && fkpos >= p.k2lo;
       const __half* fq = STAGED ? reinterpret_cast<const __half*>(&sm.stg[bf][x * a.G + g][0])
                                 : a.q + p.qoff(fit.b, fi0 + g, fit.h);
       const __half* fk2 = STAGED ? reinterpret_cast<const __half*>(&sm.stg[bf][2 * a.G + x * a.G + g + kk][0])
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_in = r < a.G * a.R && g < nq;
       const int pos = p.np + i0 + g;
       const int kpos = pos - a.R + 1 + kk;
-      const bool valid = row_in && kpos >= 0;
+      const bool valid = row_in && kpos >= p.k2lo;
       const int srow = x * a.G + g + kk;  // this row's k2/v2 staging offset
       const __half* qrow = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][x * a.G + g][0])
                                   : a.q + p.qoff(it.b, i0 + g, it.h);
@@ -834,14 +835,38 @@ bool tc_fwd_supported(const Problem& p) {
   return (p.D == 64 || p.D == 128) && w2 >= 1 && w2 <= 128;
 }
 
+// Window split (sa_split.cu) of a long folded window: sub-problems of <= 32 K' rows whose (o_b, lse_b)
+// are merged exactly.  Taken for w2 > 64, and for w2 > 32 when the long window is short (w1 <= 256):
+// at w2 = 64 the single tiling runs as fast as the split once w1 >= 512, where the chunk loop
+// amortises its epilogue (Table 1 sweep).  SA_FWD_WSPLIT=1 splits any
+// w2 > 32, SA_NO_WSPLIT=1 never splits.
+static int fwd_split_count(const Problem& p) {
+  static const bool off = getenv("SA_NO_WSPLIT") && atoi(getenv("SA_NO_WSPLIT")) != 0;
+  static const bool all = getenv("SA_FWD_WSPLIT") && atoi(getenv("SA_FWD_WSPLIT")) != 0;
+  const int w2 = swapped(p) ? p.w1 : p.w2, w1 = swapped(p) ? p.w2 : p.w1;
+  if (off || w2 <= 32) return 1;
+  if (w2 <= 64 && w1 > 256 && !all) return 1;
+  return (w2 + 31) / 32;
+}
+static size_t fa256(size_t x) { return (x + 255) & ~size_t(255); }
+
 size_t tc_fwd_workspace_bytes(const Problem& p) {
   const size_t n = p.nkey(), nq = size_t(p.B) * p.N * p.H * p.D;
-  return 3 * ((n * 2 + 255) & ~size_t(255)) + ((nq * 2 + 255) & ~size_t(255));
+  const int ns = fwd_split_count(p);
+  // split partials: ns o_b (fp32, nq floats each) then ns lse_b (B H N floats each), packed
+  const size_t parts = ns > 1 ? fa256(4 * size_t(ns) * nq) + fa256(4 * size_t(ns) * p.B * p.H * p.N) : 0;
+  return 3 * fa256(n * 2) + fa256(nq * 2) + parts;
 }
+
+static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, const char* vf, const char* k2f,
+                            const char* qf, const void* v2, void* o, float* lse, cudaStream_t st);
+cudaError_t split_merge(const float* ob, const float* lb, int nsplit, const Problem& p, void* o, float* lse,
+                        bool out_f32, cudaStream_t st);
 
 cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const void* k, const void* v,
                           const void* k2, const void* v2, void* o, float* lse, void* ws, cudaStream_t st) {
   Problem p = p0;
+  const int ns = fwd_split_count(p0);
   if (swapped(p)) {  // fold the smaller-window key into the query (exact symmetry; det negates)
     std::swap(k, k2);
     std::swap(v, v2);
@@ -851,12 +876,35 @@ cudaError_t tc_forward_ws(const Problem& p0, bool out_f32, const void* q, const 
   const size_t n = p.nkey();
   const size_t nq = size_t(p.B) * p.N * p.H * p.D;
   char* kf = (char*)ws;
-  char* vf = kf + ((n * 2 + 255) & ~size_t(255));
-  char* k2f = vf + ((n * 2 + 255) & ~size_t(255));
-  char* qf = k2f + ((n * 2 + 255) & ~size_t(255));
+  char* vf = kf + fa256(n * 2);
+  char* k2f = vf + fa256(n * 2);
+  char* qf = k2f + fa256(n * 2);
   cudaError_t e = convert_pair_f16(k, kf, v, vf, int64_t(n), num_sms(), st);
   if (e == cudaSuccess) e = convert_two_f16(q, qf, int64_t(nq), k2, k2f, int64_t(n), num_sms(), st);
   if (e != cudaSuccess) return e;
+  if (ns == 1) return fwd_core(p, out_f32, kf, vf, k2f, qf, v2, o, lse, st);
+  // window split: sub-problem b (K' offsets [32 b, 32 b + w_b) back from the query) sees K', V'
+  // through pointers shifted by -32 b rows; its (o_b fp32, lse_b) are merged exactly
+  char* parts = qf + fa256(nq * 2);
+  const size_t nl = size_t(p.B) * p.H * p.N;
+  const int64_t kstep = int64_t(p.Hk) * p.D;
+  for (int b = 0; b < ns && e == cudaSuccess; ++b) {
+    Problem sp = p;
+    sp.k2lo = 32 * b;
+    sp.w2 = std::min(32, p.w2 - 32 * b);
+    float* ob = (float*)parts + size_t(b) * nq;
+    float* lb = (float*)(parts + fa256(4 * size_t(ns) * nq)) + size_t(b) * nl;
+    e = fwd_core(sp, true, kf, vf, (const char*)((const __half*)k2f - sp.k2lo * kstep),
+                 qf, (const __nv_bfloat16*)v2 - sp.k2lo * kstep, ob, lb, st);
+  }
+  if (e == cudaSuccess)
+    e = split_merge((const float*)parts, (const float*)(parts + fa256(4 * size_t(ns) * nq)), ns, p, o, lse, out_f32,
+                    st);
+  return e;
+}
+
+static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, const char* vf, const char* k2f,
+                            const char* qf, const void* v2, void* o, float* lse, cudaStream_t st) {
   CUtensorMap tmK, tmV;
   if (!make_tmap_bnhd_f16(&tmK, kf, p.B, p.NK(), p.Hk, p.D, kChunk) ||
       !make_tmap_bnhd_f16(&tmV, vf, p.B, p.NK(), p.Hk, p.D, kChunk))

@@ -95,6 +95,10 @@ def test_fp32_shapes(B, N, H, D, w1, w2, det):
     (2, 150, 1, 128, 64, 1),     # w2 = 1 (R = 1, G = 128): forward generic epilogue; backward tiles of R = 2
     (1, 200, 1, 128, 96, 40),    # R = 40: forward G = 3; backward pads each query to 64 rows
     (1, 100, 2, 64, 24, 3),      # R = 3, D = 64: backward pads to 4 rows
+    # window split: w2 > 32 runs as sub-windows of <= 32 K' rows
+    (1, 300, 1, 128, 64, 96),    # 3 sub-windows of 32, forward and backward split
+    (1, 300, 2, 128, 600, 72),   # w1 clamps to 300 (> 256): forward R = 72 unsplit, backward 32 + 32 + 8
+    (1, 250, 1, 64, 100, 200),   # swapped: folded window 100 = 32 + 32 + 32 + 4, D = 64
 ])
 def test_bf16_shapes(B, N, H, D, w1, w2, det, force_simt):
     inp = make_inputs(B, N, H, D, seed=7 * N + D, dtype="bf16")
@@ -301,6 +305,7 @@ def test_match3_det_kernel(dtype):
     (4, 2, 128, 96, 32, False),   # tcgen05 path, ratio 2
     (8, 1, 64, 64, 16, True),     # all query heads share one key head (det)
     (4, 4, 128, 64, 32, False),   # H_kv == H: the ordinary path through the GQA entry points
+    (4, 2, 128, 80, 70, True),    # window split with grouped keys (sub-windows 32 + 32 + 6), det
 ])
 def test_gqa(dtype, tol, H, Hk, D, w1, w2, det):
     """Grouped-query entry points against the grouped-query oracle (expand + group sums)."""
@@ -376,3 +381,34 @@ def test_r128_backward_on_tcgen05(det):
     """w2 = 128 (Table 1's (128, 128) row) runs the tcgen05 backward, not the CUDA-core path."""
     assert sa.bwd_path(1, 16, 8192, 128, 128, 128, det=det) == sa.SA_PATH_TCGEN05
     assert sa.fwd_path(1, 16, 8192, 128, 128, 128, det=det) == sa.SA_PATH_TCGEN05
+
+
+@pytest.mark.parametrize("det", [False, True])
+def test_unsplit_tiling(det):
+    """SA_NO_WSPLIT=1 (read once per process) keeps the single R = 64 / 128 tilings of the folded
+    window instead of the window split: run them in a child process against the oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import json, sys
+sys.path[:0] = {[os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__))]!r}
+from sa_testutil import maxabs
+from test_parity_gpu import run_cuda, run_oracle
+from paper_2507_02754_b200.inputs import make_inputs
+out = {{}}
+for (N, w1, w2) in ((300, 128, 64), (200, 64, 128)):
+    inp = make_inputs(1, N, 2, 128, seed=N, dtype="bf16")
+    got = run_cuda(inp, w1, w2, {det})
+    ref = run_oracle(inp, w1, w2, {det})
+    out[f"{{w1}}x{{w2}}"] = {{n: maxabs(got[n], ref[n]) for n in got}}
+print(json.dumps(out))
+"""
+    env = dict(os.environ, SA_NO_WSPLIT="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for shape, errs in res.items():
+        record_errors(errs, TOL_BF16, tag=f"test_unsplit_tiling[{det}]::{shape}")
+        assert all(e <= TOL_BF16 for e in errs.values()), (shape, errs)
