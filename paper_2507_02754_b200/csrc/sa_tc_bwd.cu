@@ -1902,87 +1902,52 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           *reinterpret_cast<uint4*>(sm.adp[buf] + dst) = od;
         }
         if (DET) {
-          // A_S = k2 x q (chunkwise cross products; trailing D mod 3 dims 0): tasks (row pair (r, r+1)
-          // of one query, 24-column block).  The query's q block is converted once for both rows and
-          // the two rows' cross products run as packed fp32x2 arithmetic (FMUL2 / FFMA2).
-          constexpr int D3 = (D / 3) * 3;
+          // A_S = k2 x q = P1(k2) o P2(q) - P2(k2) o P1(q) per 3-chunk (sa_tc_rows.cuh perm3_*): tasks
+          // (quad of tile rows of one query (R >= kRB8 >= 4), 24-column block); the query's permuted q
+          // block is formed once per task, each row costs 3 LDS, 24 PRMT, 12 HMUL2 + 12 HFMA2, 3 STS.
           constexpr int kNBlk = (D + 23) / 24;
-          for (int task = ft; task < 64 * kNBlk; task += kNF) {
-            const int rp = task / kNBlk, e0 = (task - rp * kNBlk) * 24;
-            const int r = 2 * rp;  // rows r, r+1 (R even: same query)
-            const int g2 = r >> a.lR, kk2 = r & (a.R - 1);
-            const bool qok = r < a.G * a.R && q0 + g2 < qb;
-            const bool ok0 = qok && kbase + g2 + kk2 >= p.k2lo, ok1 = qok && kbase + g2 + kk2 + 1 >= p.k2lo;
-            uint32_t pk0[12], pk1[12];
+          for (int task = ft; task < 32 * kNBlk; task += kNF) {
+            const int rq = task / kNBlk, blk = task - rq * kNBlk;
+            const int r0 = 4 * rq, e0 = 24 * blk;
+            const int g2 = r0 >> a.lR, kk2 = r0 & (a.R - 1);
+            const bool qok = r0 < a.G * a.R && q0 + g2 < qb;
+            uint32_t xw[12], x1[12], x2[12];
 #pragma unroll
-            for (int e = 0; e < 12; ++e) pk0[e] = pk1[e] = 0u;
-            if (ok0 || ok1) {
-              int sl = sbase + g2 + kk2;
-              if (sl >= a.ring) sl -= a.ring;
-              int sl1 = sl + 1;
-              if (sl1 >= a.ring) sl1 -= a.ring;
-              float xf[24];
-              float2 yf[24];  // (row r, row r+1) pairs of k2
+            for (int u = 0; u < 3; ++u) {
+              uint4 xv = make_uint4(0u, 0u, 0u, 0u);
+              if (qok && e0 + 8 * u < D) xv = *reinterpret_cast<const uint4*>(&sm.sq[buf][g2][e0 + 8 * u]);
+              xw[4 * u] = xv.x;
+              xw[4 * u + 1] = xv.y;
+              xw[4 * u + 2] = xv.z;
+              xw[4 * u + 3] = xv.w;
+            }
+            perm3_block(xw, x1, x2);
+            int sl = sbase + g2 + kk2;
+            if (sl >= a.ring) sl -= a.ring;
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4) {
+              const bool ok = qok && kbase + g2 + kk2 + u4 >= p.k2lo;
+              int su = sl + u4;
+              if (su >= a.ring) su -= a.ring;
+              uint32_t yw[12], y1[12], y2[12], aw[12];
 #pragma unroll
               for (int u = 0; u < 3; ++u) {
-                if (e0 + 8 * u < D) {
-                  const uint4 xv = *reinterpret_cast<const uint4*>(&sm.sq[buf][g2][e0 + 8 * u]);
-                  const uint4 y0 = ok0 ? *reinterpret_cast<const uint4*>(&sm.rk2[sl][e0 + 8 * u]) : make_uint4(0u, 0u, 0u, 0u);
-                  const uint4 y1 = ok1 ? *reinterpret_cast<const uint4*>(&sm.rk2[sl1][e0 + 8 * u]) : make_uint4(0u, 0u, 0u, 0u);
-                  const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, a0[4] = {y0.x, y0.y, y0.z, y0.w},
-                                 a1[4] = {y1.x, y1.y, y1.z, y1.w};
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float2 fx = __half22float2(*reinterpret_cast<const __half2*>(&xs[e]));
-                    const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&a0[e]));
-                    const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&a1[e]));
-                    xf[8 * u + 2 * e] = fx.x;
-                    xf[8 * u + 2 * e + 1] = fx.y;
-                    yf[8 * u + 2 * e] = make_float2(f0.x, f1.x);
-                    yf[8 * u + 2 * e + 1] = make_float2(f0.y, f1.y);
-                  }
-                } else {
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) {
-                    xf[8 * u + e] = 0.f;
-                    yf[8 * u + e] = make_float2(0.f, 0.f);
-                  }
-                }
+                uint4 yv = make_uint4(0u, 0u, 0u, 0u);
+                if (ok && e0 + 8 * u < D) yv = *reinterpret_cast<const uint4*>(&sm.rk2[su][e0 + 8 * u]);
+                yw[4 * u] = yv.x;
+                yw[4 * u + 1] = yv.y;
+                yw[4 * u + 2] = yv.z;
+                yw[4 * u + 3] = yv.w;
               }
+              perm3_block(yw, y1, y2);
 #pragma unroll
-              for (int c3 = 0; c3 < 24; c3 += 3) {
-                float2 r0 = make_float2(0.f, 0.f), r1 = r0, r2 = r0;
-                if (e0 + c3 + 3 <= D3) {  // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}, both rows at once
-                  const float2 q0 = make_float2(xf[c3], xf[c3]), q1 = make_float2(xf[c3 + 1], xf[c3 + 1]),
-                               q2 = make_float2(xf[c3 + 2], xf[c3 + 2]);
-                  r0 = ffma2(yf[c3 + 1], q2, fmul2(yf[c3 + 2], make_float2(-q1.x, -q1.y)));
-                  r1 = ffma2(yf[c3 + 2], q0, fmul2(yf[c3 + 0], make_float2(-q2.x, -q2.y)));
-                  r2 = ffma2(yf[c3 + 0], q1, fmul2(yf[c3 + 1], make_float2(-q0.x, -q0.y)));
-                }
-                yf[c3] = r0;
-                yf[c3 + 1] = r1;
-                yf[c3 + 2] = r2;
-              }
+              for (int i = 0; i < 12; ++i) aw[i] = cross_word(y1[i], y2[i], x1[i], x2[i]);
 #pragma unroll
-              for (int e = 0; e < 12; ++e) {
-                pk0[e] = pack_f16x2(yf[2 * e].x, yf[2 * e + 1].x);
-                pk1[e] = pack_f16x2(yf[2 * e].y, yf[2 * e + 1].y);
-              }
-              if (!ok0)
-#pragma unroll
-                for (int e = 0; e < 12; ++e) pk0[e] = 0u;
-              if (!ok1)
-#pragma unroll
-                for (int e = 0; e < 12; ++e) pk1[e] = 0u;
+              for (int u = 0; u < 3; ++u)
+                if (e0 + 8 * u < D)
+                  *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r0 + u4, e0 / 8 + u)) =
+                      make_uint4(aw[4 * u], aw[4 * u + 1], aw[4 * u + 2], aw[4 * u + 3]);
             }
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-              if (e0 + 8 * u < D) {
-                *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r, e0 / 8 + u)) =
-                    make_uint4(pk0[4 * u], pk0[4 * u + 1], pk0[4 * u + 2], pk0[4 * u + 3]);
-                *reinterpret_cast<uint4*>(sm.as[buf] + sw128_off(r + 1, e0 / 8 + u)) =
-                    make_uint4(pk1[4 * u], pk1[4 * u + 1], pk1[4 * u + 2], pk1[4 * u + 3]);
-              }
           }
         }
         SA_TRACE_AT(trf, 3, trn, t << 16 | 34 << 8);

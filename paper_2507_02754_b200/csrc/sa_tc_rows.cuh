@@ -73,6 +73,50 @@ __device__ __forceinline__ uint32_t hmul2_u32(uint32_t x, uint32_t y) {
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
+// ---- Determinant operand by 3-chunk permutations (fp16 pairs) ----
+// Within each 3-chunk, (y x x)_r = y_{r+1} x_{r+2} - y_{r+2} x_{r+1} (indices mod 3 inside the chunk),
+// i.e.  y x x = P1(y) o P2(x) - P2(y) o P1(x)  with P_S(v)_r = v_{3 floor(r/3) + (r + S) mod 3}.
+// On packed fp16 words (2 halves each) a permuted word is one PRMT of at most two source words, so a
+// row costs a byte permute per word and operand plus one HMUL2 and one HFMA2 per word -- against
+// fp32 unpack / math / repack.  Rounding: the HMUL2 product is rounded to fp16 before the HFMA2
+// (one more fp16 rounding than the fp32 formation; logit error RMS +23% on unit-normal data,
+// DESIGN.md reading R5b).  Zero words past D make the trailing D mod 3 columns 0 (reading R5).
+__host__ __device__ constexpr int perm3_src(int r, int S) { return 3 * (r / 3) + (r % 3 + S) % 3; }
+
+// Word i (index relative to a block that starts on a 3-chunk and word boundary: i compile-time after
+// unrolling) of P_S(v), from the block's words w[0..NW).  Source words beyond NW read as 0.
+template <int S, int NW>
+__device__ __forceinline__ uint32_t perm3_word(const uint32_t (&w)[NW], int i) {
+  const int s0 = perm3_src(2 * i, S), s1 = perm3_src(2 * i + 1, S);
+  const int a = s0 >> 1, b = s1 >> 1;
+  const uint32_t n0 = (s0 & 1) ? 2u : 0u;
+  const uint32_t wa = a < NW ? w[a] : 0u, wb = b < NW ? w[b] : 0u;
+  if (a == b) {
+    const uint32_t n1 = (s1 & 1) ? 2u : 0u;
+    return __byte_perm(wa, 0u, n0 | (n0 + 1) << 4 | n1 << 8 | (n1 + 1) << 12);
+  }
+  const uint32_t n1 = (s1 & 1) ? 6u : 4u;
+  return __byte_perm(wa, wb, n0 | (n0 + 1) << 4 | n1 << 8 | (n1 + 1) << 12);
+}
+
+// Both permutations of a block of NW words.
+template <int NW>
+__device__ __forceinline__ void perm3_block(const uint32_t (&w)[NW], uint32_t (&p1)[NW], uint32_t (&p2)[NW]) {
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    p1[i] = perm3_word<1>(w, i);
+    p2[i] = perm3_word<2>(w, i);
+  }
+}
+
+// One word of y x x = P1(y) o P2(x) - P2(y) o P1(x) (unscaled fp16).
+__device__ __forceinline__ uint32_t cross_word(uint32_t y1, uint32_t y2, uint32_t x1, uint32_t x2) {
+  const __half2 t = __hmul2(*reinterpret_cast<const __half2*>(&y2), *reinterpret_cast<const __half2*>(&x1));
+  const __half2 r =
+      __hfma2(*reinterpret_cast<const __half2*>(&y1), *reinterpret_cast<const __half2*>(&x2), __hneg2(t));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+
 // Determinant row operand from fp16 rows: scale * (y x x) chunkwise, trailing D mod 3 dims 0.
 template <int D>
 __device__ __forceinline__ void row_operand_from_f16(const __half* x, const __half* y, float scale,

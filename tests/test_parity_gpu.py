@@ -120,11 +120,13 @@ def test_bf16_outputs_in_bf16(det):
         assert err.max() <= TOL_BF16, n
 
 
+@pytest.mark.parametrize("win", [(40, 16), (96, 64)])  # (96, 64): window split with a halo prefix
 @pytest.mark.parametrize("det", [False, True])
 @pytest.mark.parametrize("dtype,tol", [("f32", TOL_F32), ("bf16", TOL_BF16)])
-def test_prefixed_mode(dtype, tol, det):
+def test_prefixed_mode(dtype, tol, det, win):
     """Sequence-sharded entry points: queries with a key halo as prefix, both variants."""
-    B, N, H, D, w1, w2, npf = 1, 160, 2, 64, 40, 16, 39
+    (w1, w2) = win
+    B, N, H, D, npf = 1, 160, 2, 64, max(w1, w2) - 1
     inp = make_inputs(B, N, H, D, seed=11, dtype=dtype, n_prefix=npf)
     got = run_cuda(inp, w1, w2, det, n_prefix=npf)
     ref = run_oracle(inp, w1, w2, det, n_prefix=npf)
