@@ -915,36 +915,12 @@ __device__ __forceinline__ void q_epilogue_pass_det(QSmem<D, RING, STAGED>& sm, 
   named_bar_sync(1, kQNT);
 }
 
-// Half SUB of the determinant row operand k2 x q (3-chunks, fp32 math, fp16 packed): columns
-// [D/2 SUB, D/2 SUB + D/2), computing every 3-chunk that overlaps them (compile-time column indices,
-// so the packed row stays in registers).  Columns past the last whole chunk are 0 (reading R5).
+// Half SUB of the determinant row operand k2 x q: columns [D/2 SUB, D/2 SUB + D/2), by 3-chunk
+// permutations of the packed fp16 rows (sa_tc_rows.cuh det_words_f16).  Columns past the last whole
+// chunk are 0 (reading R5).
 template <int D, int SUB>
 __device__ __forceinline__ void det_half_operand(const __half* x, const __half* y, uint32_t (&pk)[D / 4]) {
-  constexpr int DH = D / 2, D3 = (D / 3) * 3, C0 = DH * SUB, CH0 = C0 / 3;
-#pragma unroll
-  for (int cc = 0; cc < (DH + 2) / 3 + 1; ++cc) {
-    constexpr int kDummy = 0;
-    (void)kDummy;
-    const int e0 = 3 * (CH0 + cc);
-    if (e0 < C0 + DH && e0 + 3 <= D3) {
-      float xf[3], yf[3];
-#pragma unroll
-      for (int u = 0; u < 3; ++u) {
-        xf[u] = __half2float(x[e0 + u]);
-        yf[u] = __half2float(y[e0 + u]);
-      }
-      // (k2 x q)_r = k2_{r+1} q_{r+2} - k2_{r+2} q_{r+1}
-      const float av[3] = {yf[1] * xf[2] - yf[2] * xf[1], yf[2] * xf[0] - yf[0] * xf[2], yf[0] * xf[1] - yf[1] * xf[0]};
-#pragma unroll
-      for (int u = 0; u < 3; ++u) {
-        const int col = e0 + u - C0;
-        if (col >= 0 && col < DH) {
-          const uint32_t h = uint32_t(__half_as_ushort(__float2half_rn(av[u])));
-          pk[col >> 1] |= (col & 1) ? (h << 16) : h;
-        }
-      }
-    }
-  }
+  det_words_f16<D, SUB * D / 4, D / 4>(x, y, pk);
 }
 
 // Determinant epilogue at R = 32 (G = 4 queries, one per TMEM lane quarter), row-owned like

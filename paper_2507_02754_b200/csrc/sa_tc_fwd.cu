@@ -59,8 +59,8 @@ struct FwdArgs {
   float* lse;
   int out_f32;
   int R, G, ngroups, npairs, items;
-  float a_scale;  // s * log2(e), signed: applied to the det row operand
-  float sm_mult;  // softmax multiplier of the raw logits: s * log2(e) (trilinear, unscaled HMUL2 operand) or 1 (det)
+  int det_neg;    // det with a negated scale (folded window swapped): form q x k2 = -(k2 x q)
+  float sm_mult;  // softmax multiplier of the raw (unscaled) logits: |s| log2(e)
 };
 
 // exp2 on the FMA pipe for a pair (FA4-style offload of part of the MUFU work): 2^x = 2^round(x) *
@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int t = 0; t < D / 2; ++t) pk[t] = 0u;
           if (fvalid) {
             if (p.det) {
-              row_operand_from_f16<D>(fq, fk2, a.a_scale, pk);
+              if (a.det_neg)  // unscaled q x k2 (the |s| log2e scale is applied by the softmax FFMA)
+                det_words_f16<D, 0, D / 2>(fk2, fq, pk);
+              else            // unscaled k2 x q
+                det_words_f16<D, 0, D / 2>(fq, fk2, pk);
             } else {  // unscaled q o k2 (the scale is applied by the softmax FFMA)
               const uint4* xp = reinterpret_cast<const uint4*>(fq);
               const uint4* yp = reinterpret_cast<const uint4*>(fk2);
@@ -922,8 +925,8 @@ static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, cons
   a.ngroups = (p.N + a.G - 1) / a.G;
   a.npairs = (a.ngroups + 1) / 2;
   a.items = a.npairs * p.B * p.H;
-  a.a_scale = p.scale * kLog2e;
-  a.sm_mult = p.det ? 1.f : p.scale * kLog2e;
+  a.det_neg = p.det && p.scale < 0.f ? 1 : 0;
+  a.sm_mult = fabsf(p.scale) * kLog2e;
   const int grid = std::min(a.items, num_sms());
   const bool staged = 2 * a.G + 2 * (a.R + 2 * a.G - 1) <= kStgRows;
   auto launch = [&](auto kern, size_t smem) {

@@ -117,6 +117,34 @@ __device__ __forceinline__ uint32_t cross_word(uint32_t y1, uint32_t y2, uint32_
   return *reinterpret_cast<const uint32_t*>(&r);
 }
 
+// Words [W0, W0 + NWO) (compile-time; word w = columns 2w, 2w+1) of the unscaled determinant row
+// operand y x x for fp16 rows x, y of D elements (16-byte aligned, shared or global memory).
+template <int D, int W0, int NWO>
+__device__ __forceinline__ void det_words_f16(const __half* x, const __half* y, uint32_t (&out)[NWO]) {
+  constexpr int B0 = (2 * W0) / 24, B1 = (2 * (W0 + NWO) - 1) / 24;
+#pragma unroll
+  for (int b = B0; b <= B1; ++b) {
+    uint32_t xw[12], yw[12], x1[12], x2[12], y1[12], y2[12];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      uint4 xv = make_uint4(0u, 0u, 0u, 0u), yv = xv;
+      if (24 * b + 8 * u < D) {
+        xv = *reinterpret_cast<const uint4*>(x + 24 * b + 8 * u);
+        yv = *reinterpret_cast<const uint4*>(y + 24 * b + 8 * u);
+      }
+      xw[4 * u] = xv.x, xw[4 * u + 1] = xv.y, xw[4 * u + 2] = xv.z, xw[4 * u + 3] = xv.w;
+      yw[4 * u] = yv.x, yw[4 * u + 1] = yv.y, yw[4 * u + 2] = yv.z, yw[4 * u + 3] = yv.w;
+    }
+    perm3_block(xw, x1, x2);
+    perm3_block(yw, y1, y2);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const int w = 12 * b + i;
+      if (w >= W0 && w < W0 + NWO) out[w - W0] = cross_word(y1[i], y2[i], x1[i], x2[i]);
+    }
+  }
+}
+
 // Determinant row operand from fp16 rows: scale * (y x x) chunkwise, trailing D mod 3 dims 0.
 template <int D>
 __device__ __forceinline__ void row_operand_from_f16(const __half* x, const __half* y, float scale,
