@@ -1028,6 +1028,126 @@ __device__ __forceinline__ void q_epilogue_rot_det(QSmem<D, RING, STAGED>& sm, c
   }
 }
 
+// Determinant epilogue at R = 32 in four phases (the trilinear rotation of q_epilogue_rot): phase ph of
+// query g covers the 32 output columns of block (ph + g) & 3, warp m = 2 half + sub takes 8 of them
+// [cs, cs + 8).  The cross products of an output column read the other two columns of its 3-chunk,
+// which may lie outside the block: the thread loads the chunk-aligned window [c0, c0 + 12),
+// c0 = cs - cs mod 3, of W (TMEM, read-only), k2 and s q; only its own 8 dk2 / dv2 ring columns are
+// written, so the block rotation keeps rows of different queries that share a key row apart.
+//   dq_c  = s (W x k2)_c,   dk2_c += (s q x W)_c,   dv2_c += dO_c U_c   (columns >= 3 floor(D/3): dq,
+//   dk2 contributions 0, reading R5).  The window offset o = cs - c0 (warp-uniform) selects one of three
+// compile-time index maps.
+template <int O>
+__device__ __forceinline__ void det_cols8(const float (&w)[16], const float (&k2)[12], const float (&qs)[12],
+                                          float s, int c0, int d3, float (&v)[8], float (&ck)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    constexpr int kDummy = 0;
+    (void)kDummy;
+    const int t = O + j, tb = 3 * (t / 3), r = t % 3;
+    const int i1 = tb + (r + 1) % 3, i2 = tb + (r + 2) % 3;
+    const bool in = c0 + tb + 3 <= d3;
+    v[j] = in ? s * (w[i1] * k2[i2] - w[i2] * k2[i1]) : 0.f;
+    ck[j] = in ? qs[i1] * w[i2] - qs[i2] * w[i1] : 0.f;
+  }
+}
+
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_rot_det4(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                                    int half, int sub, int r, bool valid, const QRows& rw,
+                                                    uint32_t tW, uint32_t tU, int sbase) {
+  static_assert(QSmem<D, RING, STAGED>::kRing, "staged fp32 q rows");
+  constexpr int D3 = (D / 3) * 3;
+  const Problem& p = a.p;
+  const float s = p.scale;
+  const int ln = r & 31, g = r >> 5;
+  const int m = 2 * half + sub;
+  int slot = sbase + (r & 31) + g;  // key row P0 - 31 + g + kk
+  if (slot >= a.ring) slot -= a.ring;
+  auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
+  uint32_t uw[16], uu[8];
+  int cs = 32 * (g & 3) + 8 * m;
+  int c0 = cs - cs % 3;
+  tmem_ld16(tW + c0, uw);
+  tmem_ld8(tU + cs, uu);
+#pragma unroll
+  for (int ph = 0; ph < 4; ++ph) {
+    float k2v[12], qs[12];
+    float4 fd0 = make_float4(0.f, 0.f, 0.f, 0.f), fd1 = fd0;
+    float4 xk0 = fd0, xk1 = fd0, xv0 = fd0, xv1 = fd0;
+#pragma unroll
+    for (int e = 0; e < 12; ++e) k2v[e] = qs[e] = 0.f;
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < 12; ++e) {
+        if (c0 + e < D) {
+          k2v[e] = __half2float(rw.k2[c0 + e]);
+          qs[e] = rw.qf[c0 + e];  // s q (cvt_qf)
+        }
+      }
+      fd0 = *reinterpret_cast<const float4*>(rw.dOf + cs);
+      fd1 = *reinterpret_cast<const float4*>(rw.dOf + cs + 4);
+      xk0 = *reinterpret_cast<const float4*>(&ak[slot][cs]);
+      xk1 = *reinterpret_cast<const float4*>(&ak[slot][cs + 4]);
+      xv0 = *reinterpret_cast<const float4*>(&av[slot][cs]);
+      xv1 = *reinterpret_cast<const float4*>(&av[slot][cs + 4]);
+    }
+    tmem_ld_wait();
+    float w[16], v[8], ck[8], cv[8];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) w[e] = __uint_as_float(uw[e]);
+    const int o = cs - c0;
+    if (o == 0)
+      det_cols8<0>(w, k2v, qs, s, c0, D3, v, ck);
+    else if (o == 1)
+      det_cols8<1>(w, k2v, qs, s, c0, D3, v, ck);
+    else
+      det_cols8<2>(w, k2v, qs, s, c0, D3, v, ck);
+    {
+      const float fd[8] = {fd0.x, fd0.y, fd0.z, fd0.w, fd1.x, fd1.y, fd1.z, fd1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cv[e] = fd[e] * __uint_as_float(uu[e]);
+    }
+    if (valid) {
+      *reinterpret_cast<float4*>(&ak[slot][cs]) =
+          make_float4(xk0.x + ck[0], xk0.y + ck[1], xk0.z + ck[2], xk0.w + ck[3]);
+      *reinterpret_cast<float4*>(&ak[slot][cs + 4]) =
+          make_float4(xk1.x + ck[4], xk1.y + ck[5], xk1.z + ck[6], xk1.w + ck[7]);
+      *reinterpret_cast<float4*>(&av[slot][cs]) =
+          make_float4(xv0.x + cv[0], xv0.y + cv[1], xv0.z + cv[2], xv0.w + cv[3]);
+      *reinterpret_cast<float4*>(&av[slot][cs + 4]) =
+          make_float4(xv1.x + cv[4], xv1.y + cv[5], xv1.z + cv[6], xv1.w + cv[7]);
+    }
+    const int csd = cs;
+    if (ph < 3) {  // next phase's TMEM columns before this phase's reduction and barrier
+      cs = 32 * ((ph + 1 + g) & 3) + 8 * m;
+      c0 = cs - cs % 3;
+      tmem_ld16(tW + c0, uw);
+      tmem_ld8(tU + cs, uu);
+    }
+#pragma unroll
+    for (int st = 16, n = 4; st >= 4; st >>= 1, n >>= 1) {
+      const bool hi = ln & st;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+      }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int col = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+    if ((ln & 3) == 0 && g < it.nq) {
+      const int64_t off = p.qoff(it.b, it.i0 + g, it.h) + csd + col;
+      if (a.out_f32)
+        reinterpret_cast<float*>(a.dq)[off] = v[0];
+      else
+        reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(v[0]);
+    }
+    named_bar_sync(1, kQNT);
+  }
+}
+
 template <int D, bool DET, int RING, bool STAGED>
 __global__ void __launch_bounds__(kQThreads, 1)
     tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
@@ -1511,7 +1631,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
       } else if constexpr (Sm::kRot && DET) {
         const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
-        q_epilogue_rot_det<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
+        if constexpr (Sm::kRing)
+          q_epilogue_rot_det4<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
+        else
+          q_epilogue_rot_det<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase);
       } else if constexpr (Sm::kRot) {
         const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
         q_epilogue_rot<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase, tr, treg, trn,
