@@ -127,6 +127,15 @@ __device__ __forceinline__ void tma_load_4d(void* smem, const CUtensorMap* m, ui
       : "memory");
 }
 
+// 1-D bulk copy (TMA engine, no tensor map) of `bytes` (multiple of 16, both addresses 16-byte
+// aligned) into shared memory, completing as transaction bytes on `bar`.
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // ------------------------------------------------------------------------------------------
 // tcgen05: TMEM allocation, fences, MMA, commit, ld/st
 // ------------------------------------------------------------------------------------------

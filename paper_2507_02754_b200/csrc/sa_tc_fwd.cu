@@ -80,19 +80,28 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <int D>
+// RS != 0 (R in {2, 4, 8, 16}): two K/V stages (a pair spans one or two chunks) make room for the
+// epilogue's fp16 row products X (one 128 x D tile per tile of the pair, SWIZZLE_128B, MN-major A
+// operand of the reduction MMA) and the 0/1 query-selection matrix (K-major B operand, N <= 64 rows).
+template <int D, int RS>
 struct Smem {
+  static constexpr int kSt = RS ? 2 : kStages;
   static constexpr int kPanelBytes = kChunk * 128;  // 64 rows x 64 fp16
   static constexpr int kStageBytes = kChunk * D * 2;
-  alignas(1024) uint8_t k[kStages][kStageBytes];
-  alignas(1024) uint8_t v[kStages][kStageBytes];
-  float ebuf[2][128][17];
+  static constexpr int kXBytes = 128 * D * 2;
+  static constexpr int kNSel = RS == 0 ? 16 : (128 / RS < 16 ? 16 : 128 / RS);  // reduction MMA N
+  static constexpr int kSelBytes = 2 * kNSel * 128;  // 2 K-panels x kNSel query rows x 128 B
+  alignas(1024) uint8_t k[kSt][kStageBytes];
+  alignas(1024) uint8_t v[kSt][kStageBytes];
+  alignas(1024) uint8_t xr[RS ? 2 : 1][RS ? kXBytes : 16];
+  alignas(1024) uint8_t sel[RS ? kSelBytes : 16];
+  float ebuf[RS ? 1 : 2][RS ? 1 : 128][17];  // generic epilogues only
   // staged bf16 rows of the next/current pair: q (2G), k2 (R+2G-1), v2 (R+2G-1); pitch D+8
   alignas(16) __nv_bfloat16 stg[2][kStgRows][D + 8];
   float rm[2][128], rl[2][128];
   float gM[2][128], gL[2][128];
-  uint64_t kvfull[kStages], kvempty[kStages];
-  uint64_t sfull[2], pready[2], udone[2], aready[2];
+  uint64_t kvfull[kSt], kvempty[kSt];
+  uint64_t sfull[2], pready[2], udone[2], aready[2], odone[2], stgfull[2];
   uint32_t tmem_base;
 };
 
@@ -120,88 +129,22 @@ __device__ __forceinline__ int chunk_width(const Item& it, int c) {
   return ((it.span - kChunk * (it.nch - 1)) + 15) & ~15;
 }
 
-// Epilogue blocks for R in {2, 4, 8, 16} (compile-time R): a warp holds 32/R whole queries in aligned
-// groups of R lanes; the R-row sum of each 16-column block of v2 o U (weighted by the row's
-// e^{m_(i,k)-m_i}) by a reduce-scatter inside the group leaves 16/R columns per lane.  The next
-// block's TMEM columns are requested before this block's shuffles.
-template <int R, int D, bool STAGED>
-__device__ __forceinline__ void fwd_epi_small(const FwdArgs& a, const Item& it, uint32_t tU, const __nv_bfloat16* v2row,
-                                              bool valid, bool qlive, float crow, float invL, int lane, int i0, int g) {
-  constexpr int NF = 16 / R;  // columns per lane after the reduce-scatter
-  const int gl = lane & (R - 1);
-  int cbase = 0;
-#pragma unroll
-  for (int k = 0, st = R >> 1; st > 0; ++k, st >>= 1)
-    if (gl & st) cbase += 8 >> k;
-  const int64_t row_off = a.p.qoff(it.b, i0 + g, it.h) + cbase;
-  uint32_t u[16];
-  tmem_ld16(tU, u);
-#pragma unroll 1
-  for (int cb = 0; cb < D / 16; ++cb) {
-    tmem_ld_wait();
-    float v[16];
-    if (valid) {
-      const uint4* vp = reinterpret_cast<const uint4*>(v2row + 16 * cb);
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const uint4 y = vp[t];
-        const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = bf16x2_to_f2(ys[e]);
-          v[8 * t + 2 * e] = f.x * crow * __uint_as_float(u[8 * t + 2 * e]);
-          v[8 * t + 2 * e + 1] = f.y * crow * __uint_as_float(u[8 * t + 2 * e + 1]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = 0.f;
-    }
-    if (cb + 1 < D / 16) tmem_ld16(tU + 16 * (cb + 1), u);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {  // stages st = R/2, ..., 1 keeping n = 8, 4, 2, 1 values
-      constexpr int kR = R;
-      const int st = (kR >> 1) >> k, n = 8 >> k;
-      if (st > 0) {
-        const bool hi = gl & st;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < n) {
-            const float keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-          }
-        }
-      }
-    }
-    if (qlive) {
-      const int64_t off = row_off + 16 * cb;
-      if (a.out_f32) {
-#pragma unroll
-        for (int i = 0; i < NF; ++i) reinterpret_cast<float*>(a.o)[off + i] = v[i] * invL;
-      } else if constexpr (NF >= 2) {
-#pragma unroll
-        for (int i = 0; i < NF; i += 2) {
-          const __nv_bfloat162 hv = __floats2bfloat162_rn(v[i] * invL, v[i + 1] * invL);
-          *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(a.o) + off + i) = hv;
-        }
-      } else {
-        reinterpret_cast<__nv_bfloat16*>(a.o)[off] = __float2bfloat16_rn(v[0] * invL);
-      }
-    }
-  }
-}
-
 // RS: 0, or the tile's R when it is in {2, 4, 8, 16} (those epilogues are compiled into kernels of
 // their own: inlined next to the R = 32 / 64 / 128 ones they cost the larger-window kernels ~4%)
 template <int D, bool STAGED, int RS>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  static_assert(sizeof(Smem<D>) + 1024 <= 232448, "shared memory budget");
-  Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw + align1024_pad(smem_raw));
+  using Sm = Smem<D, RS>;
+  static_assert(sizeof(Sm) + 1024 <= 232448, "shared memory budget");
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw + align1024_pad(smem_raw));
+  constexpr int kStages = Sm::kSt;
+  // RS kernels reduce the R rows of each query on the tensor core: O^T = X^T Sel^T (M = D rows of
+  // TMEM, N = nsel query columns, K = the 128 tile rows)
+  constexpr int kNSel = Sm::kNSel;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kPanels = D / 64;
-  constexpr uint32_t kPanelBytes = Smem<D>::kPanelBytes;
+  constexpr uint32_t kPanelBytes = Sm::kPanelBytes;
 
   if (warp == kWarpTMA && lane == 0) {
     tma_prefetch(&tmK);
@@ -215,10 +158,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.pready[x], 4);
       mbar_init(&sm.udone[x], 1);
       mbar_init(&sm.aready[x], 4);
+      mbar_init(&sm.odone[x], 1);
+      mbar_init(&sm.stgfull[x], 1);
     }
     fence_mbar_init();
   }
   if (warp == kWarpMMA) tmem_alloc<512>(&sm.tmem_base);
+  if constexpr (RS != 0) {
+    // Sel^T [nsel query rows q][128 tile rows r] = (r / RS == q), K-major SWIZZLE_128B (2 K-panels of
+    // nsel rows x 128 B); 16-byte chunk (q, c8) holds rows r = 8 c8 .. 8 c8 + 7
+    for (int t = threadIdx.x; t < kNSel * 16; t += kThreads) {
+      const int q = t >> 4, c8 = t & 15;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r0 = 8 * c8 + 2 * e;
+        const uint32_t lo = (r0 / RS == q) ? 0x3C00u : 0u, hi = ((r0 + 1) / RS == q) ? 0x3C00u : 0u;  // fp16 1.0
+        w[e] = lo | (hi << 16);
+      }
+      *reinterpret_cast<uint4*>(sm.sel + (c8 >> 3) * (kNSel * 128) + q * 128 + (((c8 & 7) ^ (q & 7)) << 4)) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -235,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (kc / kStages) & 1;
           const int row = it.jbeg + c * kChunk;
           mbar_wait(&sm.kvempty[s], ph ^ 1);
-          mbar_expect_tx(&sm.kvfull[s], 2 * Smem<D>::kStageBytes);
+          mbar_expect_tx(&sm.kvfull[s], 2 * Sm::kStageBytes);
           for (int pn = 0; pn < kPanels; ++pn) {
             tma_load_4d(sm.k[s] + pn * kPanelBytes, &tmK, &sm.kvfull[s], pn * 64, it.hk, row, it.b);
             tma_load_4d(sm.v[s] + pn * kPanelBytes, &tmV, &sm.kvfull[s], pn * 64, it.hk, row, it.b);
@@ -248,34 +210,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc_pv = idesc_f16(128, D, 0, 1);
     uint32_t kc = 0, gc = 0;
     int trn = 0;
+    // S MMAs of chunk c of item `jt` (ring position kc0 + c) into tile x's S columns
+    auto issue_s = [&](const Item& jt, uint32_t kc0, int c, int x) {
+      const int s = (kc0 + c) % kStages;
+      const uint32_t idesc_s = idesc_f16(128, chunk_width(jt, c), 0, 0);
+      const uint64_t dk = smem_desc_sw128(smem_u32(sm.k[s]), 16, 1024);
+      if (elect_one()) {  // one thread issues the group (descriptors advance in uniform registers)
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+          mma_ts(tbase + kColS0 + 64 * x, tbase + kColA0 + 64 * x + kk * 8, desc_adv(dk, off), idesc_s,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.sfull[x]);
+      }
+      __syncwarp();
+    };
+    // A operands of both tiles of item `jt` formed (the 8 softmax warps bar.arrive on named barriers
+    // 6/7, the MMA warp blocks in bar.sync: no mbarrier polling), then its chunk-0 S MMAs
+    auto first_s = [&](const Item& jt, uint32_t kc0) {
+      named_bar_sync(6, 4 * 32 + 32);
+      named_bar_sync(7, 4 * 32 + 32);
+      mbar_wait(&sm.kvfull[kc0 % kStages], (kc0 / kStages) & 1);
+      tc_fence_after();
+      issue_s(jt, kc0, 0, 0);
+      issue_s(jt, kc0, 0, 1);
+    };
+    if (blockIdx.x < a.items) first_s(get_item(a, blockIdx.x), 0);
     for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
       const Item it = get_item(a, item);
       const int tn = item / gridDim.x;
       const bool trm = lane == 0 && tn >= 50 && tn < 52;
-      auto issue_s = [&](int c, int x) {
-        const int s = (kc + c) % kStages;
-        const uint32_t idesc_s = idesc_f16(128, chunk_width(it, c), 0, 0);
-        const uint64_t dk = smem_desc_sw128(smem_u32(sm.k[s]), 16, 1024);
-        if (elect_one()) {  // one thread issues the group (descriptors advance in uniform registers)
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
-            mma_ts(tbase + kColS0 + 64 * x, tbase + kColA0 + 64 * x + kk * 8, desc_adv(dk, off), idesc_s,
-                   kk > 0 ? 1u : 0u);
-          }
-          mma_commit(&sm.sfull[x]);
-        }
-        __syncwarp();
-      };
-      // A operands of both tiles formed: the 8 softmax warps bar.arrive on named barriers 6/7, the MMA
-      // warp blocks in bar.sync (no mbarrier polling)
-      named_bar_sync(6, 4 * 32 + 32);
-      named_bar_sync(7, 4 * 32 + 32);
       SA_TRACE_AT(trm, 0, trn, tn << 16 | 10 << 8);
-      mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(0, 1);
+      if constexpr (RS == 0) {
+        if (item != int(blockIdx.x)) first_s(it, kc);
+      }
       for (int c = 0; c < it.nch; ++c) {
         const int s = (kc + c) % kStages;
         const int w = chunk_width(it, c);
@@ -297,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_wait(&sm.kvfull[(kc + c + 1) % kStages], ((kc + c + 1) / kStages) & 1);
               tc_fence_after();
             }
-            issue_s(c + 1, x);
+            issue_s(it, kc, c + 1, x);
           }
         }
         mma_commit_w(&sm.kvempty[s]);
@@ -306,6 +275,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit_w(&sm.udone[1]);
       kc += it.nch;
       ++gc;
+      if constexpr (RS != 0) {
+        // the next item's chunk-0 S MMAs go first (its A operands are formed before this item's
+        // epilogue), then the two row-group reductions O^T = X^T Sel^T of this item's epilogue into
+        // the first kNSel columns of each tile's U (read out before X was published)
+        const int nitem = item + int(gridDim.x);
+        if (nitem < a.items) first_s(get_item(a, nitem), kc);
+        const uint32_t idesc_r = idesc_f16(128, kNSel, 1, 0);
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          named_bar_sync(8 + x, 4 * 32 + 32);  // X of tile x in shared memory (4 epilogue warps arrive)
+          tc_fence_after();
+          const uint64_t dx = smem_desc_sw128(smem_u32(sm.xr[x]), 128 * 128, 1024);
+          const uint64_t ds = smem_desc_sw128(smem_u32(sm.sel), 16, 1024);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)  // K = 128 tile rows, 16 per instruction
+              mma_ss(tbase + kColU0 + 128 * x, desc_adv(dx, kk * 16 * 128),
+                     desc_adv(ds, (kk / 4) * (kNSel * 128) + (kk % 4) * 32), idesc_r, kk > 0 ? 1u : 0u);
+            mma_commit(&sm.odone[x]);
+          }
+          __syncwarp();
+        }
+      }
     }
   } else {
     // ------------------------------ softmax + epilogue of tile x = warp / 4 ------------------------------
@@ -327,6 +319,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i0 = 2 * it.pair * a.G;
       const int kb = p.np + i0 - a.R + 1;
       const int nrows = 2 * a.G + 2 * nk2;
+      if constexpr (RS != 0) {
+        // small R: one 1-D bulk copy per row (thread `row`), completing on stgfull[buf] -- the
+        // ~1.7k 16-byte cp.async of a pair are LSU-throughput bound on the softmax warps' path
+        const void* src = nullptr;
+        const int row = tid;
+        if (row < 2 * a.G) {
+          if (i0 + row < p.N) src = a.q + p.qoff(it.b, i0 + row, it.h);
+        } else if (row < nrows) {
+          const int rr = row - 2 * a.G;
+          const int kp = kb + (rr < nk2 ? rr : rr - nk2);
+          if (kp >= p.k2lo && kp < p.NK())
+            src = rr < nk2 ? (const void*)(a.k2 + p.kvoff(it.b, kp, it.hk)) : (const void*)(a.v2 + p.kvoff(it.b, kp, it.hk));
+        }
+        // every row is copied (rows outside the problem from a valid dummy address, never read), so
+        // one thread posts the pair's whole byte count: one expect_tx instead of ~110 arrivals
+        if (row < nrows) bulk_load(&sm.stg[buf][row][0], src ? src : (const void*)a.q, 2 * D, &sm.stgfull[buf]);
+        if (tid == 0) mbar_expect_tx(&sm.stgfull[buf], uint32_t(nrows) * 2 * D);
+        return;
+      }
       for (int task = tid; task < nrows * kC8; task += 256) {
         const int row = task / kC8, c8 = task % kC8;
         const void* src = nullptr;
@@ -397,7 +408,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (blockIdx.x < a.items) {
       stage(blockIdx.x, 0);
       if (STAGED) {
-        cp_async_wait<0>();
+        if constexpr (RS != 0)
+          mbar_wait(&sm.stgfull[0], 0);
+        else
+          cp_async_wait<0>();
         named_bar_sync(3, 256);
       }
       form_A(blockIdx.x, 0);
@@ -515,7 +529,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       // ---- A operand of the next pair (its first S MMAs then run during this pair's epilogue) ----
       if (nitem < a.items) {
-        if (STAGED) cp_async_wait<0>();
+        if constexpr (RS != 0) {
+          if (STAGED) mbar_wait(&sm.stgfull[buf ^ 1], ((gc + 1) >> 1) & 1);
+        } else {
+          if (STAGED) cp_async_wait<0>();
+        }
         named_bar_sync(3, 256);  // every softmax warp is past its last S wait: the A regions are free
         form_A(nitem, buf ^ 1);
       }
@@ -525,8 +543,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 26 << 8);
       if constexpr (RS != 0) {
         // R = RS in {2, 4, 8, 16} (kernel instances of their own): a warp holds 32/R whole queries in
-        // aligned groups of R lanes; group statistics by butterfly shuffles inside the group, the R-row
-        // sum of each 16-column block by a reduce-scatter inside the group (16/R columns per lane)
+        // aligned groups of R lanes; group statistics by butterfly shuffles inside the group.  The
+        // R-row sum o_i = sum_k (e^{m_k - M} / L) v2_k o U_k runs on the tensor core: each thread writes
+        // its row's fp16 products X_r = (e^{m_r - M} / L) v2_r o U_r (zero for masked rows) into
+        // shared memory, the MMA warp computes O^T = X^T Sel^T into TMEM (lane = column d, one TMEM
+        // column per query), and each warp stores its 32 columns of every query.
         const bool live = valid && m_ref != -INFINITY;
         float M = live ? m_ref : -INFINITY;
         for (int o = RS >> 1; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
@@ -536,8 +557,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool qlive = g < nq;
         const int gl = lane & (RS - 1);  // lane within the query's group
         if (gl == 0 && qlive) a.lse[(int64_t(it.b) * p.H + it.h) * p.N + i0 + g] = (M + log2f(L)) * kLn2;
-        const float invL = qlive ? 1.f / L : 0.f;
-        fwd_epi_small<RS, D, STAGED>(a, it, tU, v2row, valid, qlive, crow, invL, lane, i0, g);
+        const float sc = (live && L > 0.f) ? crow / L : 0.f;  // L = 0: an empty sub-window (split)
+        uint8_t* xb = sm.xr[x];
+        uint32_t u[32];
+        tmem_ld32(tU, u);
+#pragma unroll
+        for (int cb = 0; cb < D / 32; ++cb) {
+          tmem_ld_wait();
+          uint32_t pk[16];
+          if (sc != 0.f) {
+            const uint4* vp = reinterpret_cast<const uint4*>(v2row + 32 * cb);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const uint4 y = vp[t];
+              const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = bf16x2_to_f2(ys[e]);
+                pk[4 * t + e] = pack_f16x2(f.x * sc * __uint_as_float(u[8 * t + 2 * e]),
+                                           f.y * sc * __uint_as_float(u[8 * t + 2 * e + 1]));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+          }
+          if (cb + 1 < D / 32) tmem_ld32(tU + 32 * (cb + 1), u);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int c8 = 4 * cb + t;  // 16-byte chunk: columns 8 c8 .. 8 c8 + 7 of row r
+            *reinterpret_cast<uint4*>(xb + (c8 >> 3) * (128 * 128) + r * 128 + (((c8 & 7) ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+        tc_fence_before();
+        named_bar_arrive(8 + x, 4 * 32 + 32);
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 30 << 8);
+        mbar_wait(&sm.odone[x], gc & 1);
+        tc_fence_after();
+        SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 31 << 8);
+        // O^T: this warp's lanes are columns d = 32 qd + lane; TMEM column q = query q of the tile
+        constexpr int kG = 128 / RS;
+        uint32_t ov[kNSel];
+        if constexpr (kNSel >= 32) {
+#pragma unroll
+          for (int t = 0; t < kNSel / 32; ++t) tmem_ld32(tU + 32 * t, *reinterpret_cast<uint32_t(*)[32]>(ov + 32 * t));
+        } else {
+          tmem_ld16(tU, ov);
+        }
+        tmem_ld_wait();
+        const int nqt = min(kG, nq);
+        const int d = 32 * qd + lane;
+        if (d < D) {
+          const int64_t off0 = p.qoff(it.b, i0, it.h) + d, qstride = int64_t(p.H) * D;
+#pragma unroll
+          for (int q = 0; q < kG; ++q) {
+            if (q < nqt) {
+              const float val = __uint_as_float(ov[q]);
+              if (a.out_f32)
+                reinterpret_cast<float*>(a.o)[off0 + q * qstride] = val;
+              else
+                reinterpret_cast<__nv_bfloat16*>(a.o)[off0 + q * qstride] = __float2bfloat16_rn(val);
+            }
+          }
+        }
       } else if (a.R == 32) {
         // one warp == one query: group statistics and the row reduction stay in the warp
         const bool live = valid && m_ref != -INFINITY;
@@ -938,13 +1022,12 @@ static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, cons
   auto pick = [&](auto dc, auto sc) {
     constexpr int Dc = decltype(dc)::value;
     constexpr bool Sc = decltype(sc)::value;
-    const size_t smem = sizeof(Smem<Dc>) + 1024;
     switch (rs) {
-      case 2: launch(tc_fwd_kernel<Dc, Sc, 2>, smem); break;
-      case 4: launch(tc_fwd_kernel<Dc, Sc, 4>, smem); break;
-      case 8: launch(tc_fwd_kernel<Dc, Sc, 8>, smem); break;
-      case 16: launch(tc_fwd_kernel<Dc, Sc, 16>, smem); break;
-      default: launch(tc_fwd_kernel<Dc, Sc, 0>, smem); break;
+      case 2: launch(tc_fwd_kernel<Dc, Sc, 2>, sizeof(Smem<Dc, 2>) + 1024); break;
+      case 4: launch(tc_fwd_kernel<Dc, Sc, 4>, sizeof(Smem<Dc, 4>) + 1024); break;
+      case 8: launch(tc_fwd_kernel<Dc, Sc, 8>, sizeof(Smem<Dc, 8>) + 1024); break;
+      case 16: launch(tc_fwd_kernel<Dc, Sc, 16>, sizeof(Smem<Dc, 16>) + 1024); break;
+      default: launch(tc_fwd_kernel<Dc, Sc, 0>, sizeof(Smem<Dc, 0>) + 1024); break;
     }
   };
   using I128 = std::integral_constant<int, 128>;

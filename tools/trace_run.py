@@ -25,16 +25,16 @@ for rep in range(2):
     o, lse = binding.forward(t["q"], t["k"], t["v"], t["k2"], t["v2"], c["w1"], c["w2"], det=c["det"])
     torch.cuda.synchronize()
     n = L.simplicial_attn_debug_trace(buf, 4096)
-    fwd = [(buf[2 * i], buf[2 * i + 1]) for i in range(n) if buf[2 * i + 1]]
+    fwd = [(buf[2 * i], buf[2 * i + 1], i // 512) for i in range(4096) if buf[2 * i + 1]]
     binding.backward(t["q"], t["k"], t["v"], t["k2"], t["v2"], o, lse, t["dO"], c["w1"], c["w2"], det=c["det"])
     torch.cuda.synchronize()
     n = L.simplicial_attn_debug_trace(buf, 4096)
-    bwd = [(buf[2 * i], buf[2 * i + 1]) for i in range(n) if buf[2 * i + 1]]
+    bwd = [(buf[2 * i], buf[2 * i + 1], i // 512) for i in range(4096) if buf[2 * i + 1]]
 for name, ev in (("fwd", fwd), ("bwd", bwd)):
     if not ev:
         continue
     ev.sort(key=lambda x: x[1])
     t0 = ev[0][1]
     print(f"== {name}: {len(ev)} events")
-    for tag, clk in ev[:400]:
-        print(f"  {clk - t0:9d}  item {tag >> 16}  tag {(tag >> 8) & 0xff:3d}  c {tag & 0xff}")
+    for tag, clk, reg in ev[:400]:
+        print(f"  {clk - t0:9d}  r{reg} item {tag >> 16}  tag {(tag >> 8) & 0xff:3d}  c {tag & 0xff}")
