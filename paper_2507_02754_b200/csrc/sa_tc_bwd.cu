@@ -95,11 +95,15 @@ struct QSmem {
   static constexpr bool kGR = RING == 129;
   static constexpr bool kG1 = RING == 130;
   static constexpr bool kRot = RING == 37 || RING == 67;
+  // 38: R in {8, 16} trilinear, staged: the epilogue's row-group sums on the tensor core
+  // (q_epilogue_tc): one fp16 product tile X and the query / key-slot selection matrices
+  static constexpr bool kTC = RING == 38;
   static constexpr int kStages = kG1 ? 2 : kRot ? 4 : 3;
   static constexpr int kPanelBytes = kQChunk * 128;
   static constexpr int kStageBytes = kQChunk * D * 2;
   static constexpr int kAP = kGR ? D : D + 4;  // ring pitch (floats): padded for row-owned float4 updates
-  static constexpr int kEB = (kG1 || kRot) ? 1 : 128;  // eb rows (unused by the row-owned passes)
+  static constexpr int kEB = (kG1 || kRot || kTC) ? 1 : 128;  // eb rows (unused by the row-owned passes)
+  static constexpr int kSelRows = 48;  // Sel_q^T rows 0..15 (queries), Sel_k^T rows 16..47 (key slots)
   alignas(1024) uint8_t k[kStages][kStageBytes];
   alignas(1024) uint8_t v[kStages][kStageBytes];
   alignas(16) float acc_k2[kGR ? 1 : RING][kAP];
@@ -127,7 +131,12 @@ struct QSmem {
   alignas(16) __half rv2[kRing ? 2 : 1][kRing ? kKR : 1][D + 8];
   float slse[2][16], sdl[2][16];
   float dqx[2][32];  // R = 64: the odd lane quarter's dq column partials of the current pass
-  float dq4[4][D];  // R = 64 / 128 trilinear: per-lane-quarter dq partials
+  float dq4[kTC ? 1 : 4][D];  // R = 64 / 128 trilinear: per-lane-quarter dq partials
+  // X (fp16, SWIZZLE_128B, MN-major A); two 64-column panels even at D = 64, since the M = 128 MMA
+  // reads both (the second panel's lanes are ignored)
+  alignas(1024) uint8_t xr[kTC ? 128 * 128 * 2 : 16];
+  alignas(1024) uint8_t sel[kTC ? 2 * kSelRows * 128 : 16];   // Sel^T (K-major B, two 64-row K panels)
+  uint64_t red;  // kTC: completion of the epilogue's reduction MMAs (three per tile)
   uint64_t kvfull[kStages], kvempty[kStages];
   uint64_t sfull[2], pready[2], udone, aready;
   uint32_t tmem_base;
@@ -1148,6 +1157,126 @@ __device__ __forceinline__ void q_epilogue_rot_det4(QSmem<D, RING, STAGED>& sm, 
   }
 }
 
+// R in {8, 16} trilinear epilogue on the tensor core (RING 38).  The three row-group sums of a tile,
+//   dq_g   = sum_{kk}        X1_(g,kk),   X1 = s k2 o W      (rows of query g)
+//   dk2_k += sum_{g+kk = k}  X2_(g,kk),   X2 = s q o W       (rows sharing key slot k)
+//   dv2_k += sum_{g+kk = k}  X3_(g,kk),   X3 = dO o U
+// run as MMAs  Y^T = X^T Sel^T  (M = D TMEM lanes, N = 16 query / 32 key-slot columns, K = the 128
+// tile rows) with constant 0/1 selection matrices, one shared X tile rewritten per product (the MMA
+// warp issues each after named barrier 5 and commits to `red`).  Results land in the tile's W
+// columns (read out before X1 is published): dq^T at [0, 16), dk2^T at [32, 64), dv2^T at [64, 96).
+// X is rounded to fp16 (reading R25).  Thread (row r, warp m = 2 half + sub) owns columns
+// [m D/4, (m+1) D/4) of its row; afterwards warp m handles query / key-slot columns j = m mod 4.
+template <int D, int RING, bool STAGED>
+__device__ __forceinline__ void q_epilogue_tc(QSmem<D, RING, STAGED>& sm, const BwdQArgs& a, const QItem& it,
+                                              int half, int sub, int r, bool valid, const QRows& rw, uint32_t tW,
+                                              uint32_t tU, int sbase, uint32_t& nred, bool tr, int treg, int& trn,
+                                              int titem) {
+  constexpr int CW = D / 4;  // columns per thread
+  const Problem& p = a.p;
+  const float s = p.scale;
+  const int m = 2 * half + sub, c0 = CW * m;
+  const int qd = r >> 5, lane = r & 31;
+  uint8_t* xb = sm.xr;
+  uint32_t uw[CW];
+  if constexpr (CW == 32)
+    tmem_ld32(tW + c0, *reinterpret_cast<uint32_t(*)[32]>(uw));
+  else
+    tmem_ld16(tW + c0, uw);
+  uint32_t k2w[CW / 2], qw[CW / 2], dw[CW / 2];
+#pragma unroll
+  for (int t = 0; t < CW / 8; ++t) {
+    uint4 a4 = make_uint4(0u, 0u, 0u, 0u), b4 = a4, c4 = a4;
+    if (valid) {
+      a4 = *reinterpret_cast<const uint4*>(rw.k2 + c0 + 8 * t);
+      b4 = *reinterpret_cast<const uint4*>(rw.q + c0 + 8 * t);
+      c4 = *reinterpret_cast<const uint4*>(rw.dO + c0 + 8 * t);
+    }
+    k2w[4 * t] = a4.x, k2w[4 * t + 1] = a4.y, k2w[4 * t + 2] = a4.z, k2w[4 * t + 3] = a4.w;
+    qw[4 * t] = b4.x, qw[4 * t + 1] = b4.y, qw[4 * t + 2] = b4.z, qw[4 * t + 3] = b4.w;
+    dw[4 * t] = c4.x, dw[4 * t + 1] = c4.y, dw[4 * t + 2] = c4.z, dw[4 * t + 3] = c4.w;
+  }
+  tmem_ld_wait();
+  // X = (f16 row y) o (fp32 TMEM columns u) * sc, stored as this row's 16-byte chunks c0/8 ...
+  auto put = [&](const uint32_t* y, const uint32_t* u, float sc) {
+    uint32_t pk[CW / 2];
+#pragma unroll
+    for (int e = 0; e < CW / 2; ++e) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&y[e]));
+      pk[e] = pack_f16x2(sc * f.x * __uint_as_float(u[2 * e]), sc * f.y * __uint_as_float(u[2 * e + 1]));
+    }
+#pragma unroll
+    for (int t = 0; t < CW / 8; ++t) {
+      const int c8 = c0 / 8 + t;
+      *reinterpret_cast<uint4*>(xb + (c8 >> 3) * (128 * 128) + r * 128 + (((c8 & 7) ^ (r & 7)) << 4)) =
+          make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    named_bar_arrive(5, kQNT + 32);
+  };
+  auto wait_red = [&]() {
+    mbar_wait(&sm.red, nred & 1);
+    ++nred;
+  };
+  put(k2w, uw, s);  // X1 = s k2 o W  -> dq
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 15 << 8);
+  wait_red();
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 16 << 8);
+  put(qw, uw, s);   // X2 = s q o W   -> dk2
+  if constexpr (CW == 32)
+    tmem_ld32(tU + c0, *reinterpret_cast<uint32_t(*)[32]>(uw));
+  else
+    tmem_ld16(tU + c0, uw);
+  tmem_ld_wait();
+  wait_red();
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 17 << 8);
+  put(dw, uw, 1.f);  // X3 = dO o U   -> dv2
+  wait_red();
+  tc_fence_after();
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 18 << 8);
+  // results: lane = column d of this lane quarter; warp m takes queries [4m, 4m + 4) and key slots
+  // [8m, 8m + 8) (eight TMEM columns of each result: few live registers)
+  const int d = 32 * qd + lane;
+  uint32_t yq[8], yk[8], yv[8];
+  tmem_ld8(tW + 4 * m, yq);
+  tmem_ld8(tW + 32 + 8 * m, yk);
+  tmem_ld8(tW + 64 + 8 * m, yv);
+  tmem_ld_wait();
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 19 << 8);
+  if (d < D) {
+    const int64_t qstride = int64_t(p.H) * D;
+    const int64_t off0 = p.qoff(it.b, it.i0, it.h) + d + 4 * m * qstride;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (4 * m + j < it.nq) {
+        const float y = __uint_as_float(yq[j]);
+        if (a.out_f32)
+          reinterpret_cast<float*>(a.dq)[off0 + j * qstride] = y;
+        else
+          reinterpret_cast<__nv_bfloat16*>(a.dq)[off0 + j * qstride] = __float2bfloat16_rn(y);
+      }
+    }
+    const int P0 = p.np + it.i0;
+    const int nsl = a.R + it.nq - 1;
+    auto ak = q_acc(sm, a, 0), av = q_acc(sm, a, 1);
+    int slot = sbase + 8 * m;
+    if (slot >= a.ring) slot -= a.ring;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = 8 * m + j;
+      if (k < nsl && P0 - a.R + 1 + k >= p.k2lo) {
+        ak[slot][d] += __uint_as_float(yk[j]);
+        av[slot][d] += __uint_as_float(yv[j]);
+      }
+      if (++slot == a.ring) slot = 0;
+    }
+  }
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 20 << 8);
+  named_bar_sync(1, kQNT);  // ring rows complete before the flush
+  SA_TRACE_AT(tr, treg, trn, titem << 16 | 21 << 8);
+}
+
 template <int D, bool DET, int RING, bool STAGED>
 __global__ void __launch_bounds__(kQThreads, 1)
     tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
@@ -1176,9 +1305,32 @@ __global__ void __launch_bounds__(kQThreads, 1)
     }
     mbar_init(&sm.udone, 1);
     mbar_init(&sm.aready, kQCW);
+    mbar_init(&sm.red, 1);
     fence_mbar_init();
   }
   if (warp == kQWarpMMA) tmem_alloc<512>(&sm.tmem_base);
+  if constexpr (Sm::kTC) {
+    // Sel^T, K-major SWIZZLE_128B: row n < 16 selects the rows of query n (r / R == n), row 16 + k the
+    // rows of key slot k (r / R + r mod R == k); chunk (n, c8) holds tile rows r = 8 c8 .. 8 c8 + 7
+    for (int t = threadIdx.x; t < Sm::kSelRows * 16; t += kQThreads) {
+      const int n = t >> 4, c8 = t & 15;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t h[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int rr = 8 * c8 + 2 * e + u, g = rr >> a.lR, kk = rr & (a.R - 1);
+          const bool on = n < 16 ? g == n : g + kk == n - 16;
+          h[u] = on ? 0x3C00u : 0u;  // fp16 1.0
+        }
+        w[e] = h[0] | (h[1] << 16);
+      }
+      *reinterpret_cast<uint4*>(sm.sel + (c8 >> 3) * (Sm::kSelRows * 128) + n * 128 + (((c8 & 7) ^ (n & 7)) << 4)) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    fence_proxy_async_smem();
+  }
   for (int e = threadIdx.x; e < a.ring * Sm::kAP; e += kQThreads) {
     (&q_acc(sm, a, 0)[0][0])[e] = 0.f;
     (&q_acc(sm, a, 1)[0][0])[e] = 0.f;
@@ -1215,43 +1367,49 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const uint32_t idesc_acc = idesc_f16(128, D, 0, 1);
       uint32_t kc = 0, gc = 0;
       int trn = 0;
+      // S / dP MMAs of chunk c, half hh of item `jt` (K/V ring position kc0 + c)
+      auto issue_s = [&](const QItem& jt, uint32_t kc0, int c, int hh) {
+        const int s = (kc0 + c) % kStages;
+        const int w = q_width(jt, c);
+        const int nwh = min(32, w - 32 * hh);
+        // one elected thread issues the group: descriptors advance by 64-bit adds in uniform registers
+        const uint64_t dk = smem_desc_sw128(smem_u32(sm.k[s]) + hh * 32 * 128, 16, 1024);
+        const uint64_t dv = smem_desc_sw128(smem_u32(sm.v[s]) + hh * 32 * 128, 16, 1024);
+        const uint32_t idesc_s = idesc_f16(128, nwh > 0 ? nwh : 16, 0, 0);
+        if (elect_one()) {
+          if (nwh > 0) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
+              mma_ts(tS + 32 * hh, tAS + kk * 8, desc_adv(dk, off), idesc_s, kk > 0 ? 1u : 0u);
+              mma_ts(tdP + 32 * hh, tAdP + kk * 8, desc_adv(dv, off), idesc_s, kk > 0 ? 1u : 0u);
+            }
+          }
+          mma_commit(&sm.sfull[hh]);
+        }
+        __syncwarp();
+      };
+      // A operands of item `jt` formed (all compute warps bar.arrive), then its chunk-0 S / dP MMAs
+      auto first_s = [&](const QItem& jt, uint32_t kc0) {
+        named_bar_sync(4, kQNT + 32);
+        tc_fence_after();
+        mbar_wait(&sm.kvfull[kc0 % kStages], (kc0 / kStages) & 1);
+        tc_fence_after();
+        issue_s(jt, kc0, 0, 0);
+        issue_s(jt, kc0, 0, 1);
+      };
       QItem it = it_begin < it_end ? q_item(a, it_begin) : QItem{};
+      if (it_begin < it_end) first_s(it, 0);
       for (int item = it_begin; item < it_end; ++item, it = q_item_next(a, it)) {
         const bool trm = lane == 0 && item - it_begin >= 100 && item - it_begin < 102;
-        named_bar_sync(4, kQNT + 32);  // A operands formed (all compute warps bar.arrive)
+        if constexpr (!Sm::kTC) {
+          if (item != it_begin) first_s(it, kc);
+        }
         SA_TRACE_AT(trm, 0, trn, (item - it_begin) << 16 | 10 << 8);
-        tc_fence_after();
         // Issue order per chunk c and half hh (hh = column halves [32hh, 32hh+32) of a 64-row chunk):
         //   S_hh(0), dP_hh(0) ... then for each c: [P_hh(c) ready] W_hh(c), U_hh(c); S_hh(c+1), dP_hh(c+1)
         // so half a's next S overlaps half b's softmax (the tensor pipe is in-order, so S_hh(c+1)
         // overwriting the TMEM that held P_hh(c) / dS_hh(c) follows the W/U MMAs that read them).
-        auto issue_s = [&](int c, int hh) {
-          const int s = (kc + c) % kStages;
-          const int w = q_width(it, c);
-          const int nwh = min(32, w - 32 * hh);
-          // one elected thread issues the group: descriptors advance by 64-bit adds in uniform registers
-          const uint64_t dk = smem_desc_sw128(smem_u32(sm.k[s]) + hh * 32 * 128, 16, 1024);
-          const uint64_t dv = smem_desc_sw128(smem_u32(sm.v[s]) + hh * 32 * 128, 16, 1024);
-          const uint32_t idesc_s = idesc_f16(128, nwh > 0 ? nwh : 16, 0, 0);
-          if (elect_one()) {
-            if (nwh > 0) {
-#pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
-                const uint32_t off = (kk / 4) * kPanelBytes + (kk % 4) * 32;
-                mma_ts(tS + 32 * hh, tAS + kk * 8, desc_adv(dk, off), idesc_s, kk > 0 ? 1u : 0u);
-                mma_ts(tdP + 32 * hh, tAdP + kk * 8, desc_adv(dv, off), idesc_s, kk > 0 ? 1u : 0u);
-              }
-            }
-            mma_commit(&sm.sfull[hh]);
-          }
-          __syncwarp();
-        };
-        {
-          mbar_wait(&sm.kvfull[kc % kStages], (kc / kStages) & 1);
-          tc_fence_after();
-          issue_s(0, 0);
-          issue_s(0, 1);
-        }
         for (int c = 0; c < it.nch; ++c) {
           const int s = (kc + c) % kStages;
           const int w = q_width(it, c);
@@ -1280,7 +1438,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
                 mbar_wait(&sm.kvfull[(kc + c + 1) % kStages], ((kc + c + 1) / kStages) & 1);
                 tc_fence_after();
               }
-              issue_s(c + 1, hh);
+              issue_s(it, kc, c + 1, hh);
             }
           }
           mma_commit_w(&sm.kvempty[s]);
@@ -1288,6 +1446,28 @@ __global__ void __launch_bounds__(kQThreads, 1)
         mma_commit_w(&sm.udone);
         kc += it.nch;
         ++gc;
+        if constexpr (Sm::kTC) {
+          // the next tile's chunk-0 S / dP MMAs first (its A operands are formed before this tile's
+          // epilogue), then the epilogue's three reductions Y^T = X^T Sel^T (q_epilogue_tc)
+          if (item + 1 < it_end) first_s(q_item_next(a, it), kc);
+          const uint64_t dx = smem_desc_sw128(smem_u32(sm.xr), 128 * 128, 1024);
+#pragma unroll 1
+          for (int k = 0; k < 3; ++k) {
+            named_bar_sync(5, kQNT + 32);  // X of product k in shared memory
+            tc_fence_after();
+            const uint32_t nsel = k == 0 ? 16u : 32u;
+            const uint64_t ds = smem_desc_sw128(smem_u32(sm.sel) + (k == 0 ? 0u : 16u * 128u), 16, 1024);
+            const uint32_t idesc_r = idesc_f16(128, nsel, 1, 0);
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                mma_ss(tW + 32 * k, desc_adv(dx, kk * 16 * 128),
+                       desc_adv(ds, (kk / 4) * (Sm::kSelRows * 128) + (kk % 4) * 32), idesc_r, kk > 0 ? 1u : 0u);
+              mma_commit(&sm.red);
+            }
+            __syncwarp();
+          }
+        }
       }
     }
   } else if (warp < kQCW) {
@@ -1386,7 +1566,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       }
       cp_async_commit();
     };
-    uint32_t kc = 0, gc = 0;
+    uint32_t kc = 0, gc = 0, nred = 0;
     int PS = 0, flush_lo = 0;
     int trn = 0;
     // ---- row operands of tile `fitem` (fp16, unscaled): half 0 -> A_S = q o k2 [det: k2 x q],
@@ -1650,6 +1830,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
               reinterpret_cast<__nv_bfloat16*>(a.dq)[off] = __float2bfloat16_rn(y);
           }
         }
+      } else if constexpr (Sm::kTC) {
+        const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
+        q_epilogue_tc<D, RING, STAGED>(sm, a, it, half, sub, r, valid, rw, tW, tU, sbase, nred, tr, treg, trn,
+                                       item - it_begin);
       } else if (DET && (a.R == 32 || a.R == 64)) {
         const int sbase = a.fd_ring.mod(p.np + it.i0 - a.R + 1 + a.ring);
 #pragma unroll 1
@@ -1694,32 +1878,40 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool start_open = PS > p.np;
       const int nrows = flush_hi - flush_lo + 1;
       const int fbase = a.fd_ring.mod(flush_lo + a.ring);
-      for (int idx = tid256; idx < nrows * D; idx += kQNT) {
-        const int kp = flush_lo + idx / D, d = idx % D;
+      // four columns per task: float4 ring traffic, 8- / 16-byte global stores
+      constexpr int kD4 = D / 4;
+      for (int idx = tid256; idx < nrows * kD4; idx += kQNT) {
+        const int kp = flush_lo + idx / kD4, d = 4 * (idx % kD4);
         if (kp < p.k2lo || kp >= p.NK()) continue;
-        int slot = fbase + idx / D;
+        int slot = fbase + idx / kD4;
         if (slot >= a.ring) slot -= a.ring;
-        const float vk = q_acc(sm, a, 0)[slot][d], vv = q_acc(sm, a, 1)[slot][d];
-        q_acc(sm, a, 0)[slot][d] = 0.f;
-        q_acc(sm, a, 1)[slot][d] = 0.f;
+        float4* pk = reinterpret_cast<float4*>(&q_acc(sm, a, 0)[slot][d]);
+        float4* pv = reinterpret_cast<float4*>(&q_acc(sm, a, 1)[slot][d]);
+        const float4 vk = *pk, vv = *pv;
+        *pk = make_float4(0.f, 0.f, 0.f, 0.f);
+        *pv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (start_open && kp < PS) {
           float* bnd = a.band + ((size_t(blockIdx.x) * 2 + 0) * 2) * (a.R - 1) * D;
           const int rr = kp - (PS - a.R + 1);
-          bnd[size_t(rr) * D + d] = vk;
-          bnd[size_t(a.R - 1 + rr) * D + d] = vv;
+          *reinterpret_cast<float4*>(bnd + size_t(rr) * D + d) = vk;
+          *reinterpret_cast<float4*>(bnd + size_t(a.R - 1 + rr) * D + d) = vv;
         } else if (end_open && kp + a.R - 1 >= PE) {
           float* bnd = a.band + ((size_t(blockIdx.x) * 2 + 1) * 2) * (a.R - 1) * D;
           const int rr = kp - (PE - a.R + 1);
-          bnd[size_t(rr) * D + d] = vk;
-          bnd[size_t(a.R - 1 + rr) * D + d] = vv;
+          *reinterpret_cast<float4*>(bnd + size_t(rr) * D + d) = vk;
+          *reinterpret_cast<float4*>(bnd + size_t(a.R - 1 + rr) * D + d) = vv;
         } else {
           const int64_t off = p.koff(it.b, kp, it.h) + d;
           if (a.out_f32) {
-            reinterpret_cast<float*>(a.dk2)[off] = vk;
-            reinterpret_cast<float*>(a.dv2)[off] = vv;
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dk2) + off) = vk;
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dv2) + off) = vv;
           } else {
-            reinterpret_cast<__nv_bfloat16*>(a.dk2)[off] = __float2bfloat16_rn(vk);
-            reinterpret_cast<__nv_bfloat16*>(a.dv2)[off] = __float2bfloat16_rn(vv);
+            const __nv_bfloat162 k01 = __floats2bfloat162_rn(vk.x, vk.y), k23 = __floats2bfloat162_rn(vk.z, vk.w);
+            const __nv_bfloat162 v01 = __floats2bfloat162_rn(vv.x, vv.y), v23 = __floats2bfloat162_rn(vv.z, vv.w);
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.dk2) + off) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&k01), *reinterpret_cast<const uint32_t*>(&k23));
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.dv2) + off) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&v01), *reinterpret_cast<const uint32_t*>(&v23));
           }
         }
       }
@@ -2707,8 +2899,12 @@ static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, cons
 #define SA_Q_LAUNCH(DD, DET, RING, STG) launch(tc_bwd_q_kernel<DD, DET, RING, STG>, sizeof(QSmem<DD, RING, STG>) + 1024)
     // row-owned epilogue, 4 K/V stages: trilinear R = 32 / 64, determinant R = 32 (q_epilogue_rot_det)
     const bool rot = p.D == 128 && (R == 32 || (!p.det && R == 64));
+    // R in {8, 16} trilinear staged: tensor-core epilogue (SA_Q_TC=0 keeps the shuffle/gather passes)
+    static const bool tc_off = getenv("SA_Q_TC") && atoi(getenv("SA_Q_TC")) == 0;
+    const bool tce = !tc_off && !p.det && staged && (R == 8 || R == 16);
 #define SA_Q_PICK(DD, DET)                                                                             \
   (gr ? SA_Q_LAUNCH(DD, DET, DET ? 129 : 130, false)                                                  \
+      : (!DET && tce) ? SA_Q_LAUNCH(DD, false, 38, true)                                              \
       : (DD == 128 && rot) ? (staged ? SA_Q_LAUNCH(DD, DET, 37, true) : SA_Q_LAUNCH(DD, DET, 67, false)) \
       : staged ? SA_Q_LAUNCH(DD, DET, 36, true) : SA_Q_LAUNCH(DD, DET, 66, false))
     if (p.D == 128) {

@@ -88,7 +88,7 @@ struct Smem {
   static constexpr int kSt = RS ? 2 : kStages;
   static constexpr int kPanelBytes = kChunk * 128;  // 64 rows x 64 fp16
   static constexpr int kStageBytes = kChunk * D * 2;
-  static constexpr int kXBytes = 128 * D * 2;
+  static constexpr int kXBytes = 128 * 128 * 2;  // two 64-column panels even at D = 64 (the M = 128 MMA reads both)
   static constexpr int kNSel = RS == 0 ? 16 : (128 / RS < 16 ? 16 : 128 / RS);  // reduction MMA N
   static constexpr int kSelBytes = 2 * kNSel * 128;  // 2 K-panels x kNSel query rows x 128 B
   alignas(1024) uint8_t k[kSt][kStageBytes];
