@@ -83,6 +83,7 @@ struct BwdQArgs {
   // R: rows per query of the tiling (a power of two >= the folded window Rt); rows with
   // kk < R - Rt lie before the window and are masked like rows before the sequence start
   int out_f32, R, lR, G, ngroups, items, per_cta, ring, Rt;
+  int tma_stage;  // RING 38: rows staged by pitched TMA boxes (H, Hk >= 2), else cp.async
   FastDiv fd_ng, fd_H, fd_ring;  // by ngroups, H, ring (per-tile index arithmetic)
 };
 
@@ -122,7 +123,7 @@ struct QSmem {
   // consecutive items stage only their G new key rows
   static constexpr bool kRing = kRot && STAGED;
   static constexpr int kKR = 40;  // ring slots per half (>= R + 2G - 1 = 39)
-  alignas(16) __half stg[(STAGED && !kRing) ? 2 : 1][(STAGED && !kRing) ? kQStageRows : 1][D + 8];
+  alignas(kTC ? 128 : 16) __half stg[(STAGED && !kRing) ? 2 : 1][(STAGED && !kRing) ? kQStageRows : 1][D + 8];
   alignas(16) __half stgq[kRing ? 2 : 1][kRing ? 8 : 1][D + 8];  // q rows 0..G-1, dO rows G..2G-1
   // the same rows in fp32 (q pre-multiplied by s) for the epilogue: converted once per tile instead
   // of once per use by each of the query's 32 rows
@@ -138,7 +139,7 @@ struct QSmem {
   alignas(1024) uint8_t sel[kTC ? 2 * kSelRows * 128 : 16];   // Sel^T (K-major B, two 64-row K panels)
   uint64_t red;  // kTC: completion of the epilogue's reduction MMAs (three per tile)
   uint64_t kvfull[kStages], kvempty[kStages];
-  uint64_t sfull[2], pready[2], udone, aready;
+  uint64_t sfull[2], pready[2], udone, aready, stgfull[2];
   uint32_t tmem_base;
 };
 
@@ -1279,7 +1280,10 @@ __device__ __forceinline__ void q_epilogue_tc(QSmem<D, RING, STAGED>& sm, const 
 
 template <int D, bool DET, int RING, bool STAGED>
 __global__ void __launch_bounds__(kQThreads, 1)
-    tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, BwdQArgs a) {
+    tc_bwd_q_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                    const __grid_constant__ CUtensorMap tmQs, const __grid_constant__ CUtensorMap tmdOs,
+                    const __grid_constant__ CUtensorMap tmK2s, const __grid_constant__ CUtensorMap tmV2s,
+                    BwdQArgs a) {
   using Sm = QSmem<D, RING, STAGED>;
   extern __shared__ uint8_t smem_raw[];
   static_assert(sizeof(Sm) + 1024 <= 232448, "shared memory budget");
@@ -1306,6 +1310,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
     mbar_init(&sm.udone, 1);
     mbar_init(&sm.aready, kQCW);
     mbar_init(&sm.red, 1);
+    mbar_init(&sm.stgfull[0], 1);
+    mbar_init(&sm.stgfull[1], 1);
     fence_mbar_init();
   }
   if (warp == kQWarpMMA) tmem_alloc<512>(&sm.tmem_base);
@@ -1542,6 +1548,19 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int P0 = p.np + it.i0;
       const int nk = a.R + a.G - 1;
       const int nrows = 2 * a.G + 2 * nk;
+      if (Sm::kTC && a.tma_stage) {
+        // four pitched-row TMA boxes (q, dO: G rows; k2, v2: nk rows, the v2 box from a row that is a
+        // multiple of 8 so it starts 128-byte aligned), completing on stgfull[buf]; k2 / v2 in real
+        // rows (virtual row kp is kp - k2lo); lse / delta by cp.async below
+        if (tid256 == 0) {
+          const int kb = P0 - a.R + 1 - p.k2lo;
+          mbar_expect_tx(&sm.stgfull[buf], uint32_t(2 * a.G + 2 * nk) * (D + 8) * 2);
+          tma_load_4d(&sm.stg[buf][0][0], &tmQs, &sm.stgfull[buf], it.h * D, it.i0, it.b, 0);
+          tma_load_4d(&sm.stg[buf][a.G][0], &tmdOs, &sm.stgfull[buf], it.h * D, it.i0, it.b, 0);
+          tma_load_4d(&sm.stg[buf][2 * a.G][0], &tmK2s, &sm.stgfull[buf], it.hk * D, kb, it.b, 0);
+          tma_load_4d(&sm.stg[buf][2 * a.G + ((nk + 7) & ~7)][0], &tmV2s, &sm.stgfull[buf], it.hk * D, kb, it.b, 0);
+        }
+      } else
       for (int task = tid256; task < nrows * kC8; task += kQNT) {
         const int row = task / kC8, c8 = task % kC8;
         const __half* src = nullptr;
@@ -1591,7 +1610,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           fr.q = &sm.stg[bf][g][0];
           fr.dO = &sm.stg[bf][a.G + g][0];
           fr.k2 = &sm.stg[bf][2 * a.G + g + kk][0];
-          fr.v2 = &sm.stg[bf][2 * a.G + nk + g + kk][0];
+          fr.v2 = &sm.stg[bf][2 * a.G + ((Sm::kTC && a.tma_stage) ? ((nk + 7) & ~7) : nk) + g + kk][0];
         } else {
           fr.q = a.q + p.qoff(fi.b, fi.i0 + g, fi.h);
           fr.dO = a.dO + p.qoff(fi.b, fi.i0 + g, fi.h);
@@ -1669,6 +1688,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       stage(itc, it_begin, 0);
       if (STAGED) {
         cp_async_wait<0>();
+        if (Sm::kTC && a.tma_stage) mbar_wait(&sm.stgfull[0], 0);
         named_bar_sync(1, kQNT);
       }
       cvt_qf(0);
@@ -1722,7 +1742,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           rw.q = &sm.stg[buf][g][0];
           rw.dO = &sm.stg[buf][a.G + g][0];
           rw.k2 = &sm.stg[buf][2 * a.G + g + kk][0];
-          rw.v2 = &sm.stg[buf][2 * a.G + nk + g + kk][0];
+          rw.v2 = &sm.stg[buf][2 * a.G + ((Sm::kTC && a.tma_stage) ? ((nk + 7) & ~7) : nk) + g + kk][0];
         } else {
           rw.q = a.q + p.qoff(it.b, it.i0 + g, it.h);
           rw.dO = a.dO + p.qoff(it.b, it.i0 + g, it.h);
@@ -1787,6 +1807,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       // ---- A operands of the next tile (its S/dP MMAs then run during this tile's epilogue) ----
       if (item + 1 < it_end) {
         if (STAGED) cp_async_wait<0>();
+        if (Sm::kTC && a.tma_stage) mbar_wait(&sm.stgfull[buf ^ 1], ((gc + 1) >> 1) & 1);
         named_bar_sync(1, kQNT);  // every warp is past its last S/dP wait: the A regions are free
         cvt_qf(buf ^ 1);
         form_A(itn, item + 1, STAGED ? (buf ^ 1) : 0);
@@ -2860,6 +2881,7 @@ static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, cons
     a.dv2 = dv2;
     a.band = band;
     a.gring = gring;
+    a.tma_stage = 0;
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
     a.Rt = Rt;
@@ -2888,10 +2910,11 @@ static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, cons
     }
     {
     const int grid = q_grid(p, R, G, &a.per_cta, &a.items);
+    CUtensorMap tmQs = tmK, tmdOs = tmK, tmK2s = tmK, tmV2s = tmK;  // RING 38 row staging (below)
     auto launch = [&](auto kern, size_t smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       KernelScope ks("tc_bwd_q", st);
-      kern<<<grid, kQThreads, smem, st>>>(tmK, tmV, a);
+      kern<<<grid, kQThreads, smem, st>>>(tmK, tmV, tmQs, tmdOs, tmK2s, tmV2s, a);
     };
     // staged rows: q, dO (G each) + k2, v2 (R+G-1 each) double-buffered; the ring holds R+G rows
     const bool staged = G <= 16 && 2 * G + 2 * (R + G - 1) <= kQStageRows && R + G <= 36;
@@ -2902,6 +2925,16 @@ static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, cons
     // R in {8, 16} trilinear staged: tensor-core epilogue (SA_Q_TC=0 keeps the shuffle/gather passes)
     static const bool tc_off = getenv("SA_Q_TC") && atoi(getenv("SA_Q_TC")) == 0;
     const bool tce = !tc_off && !p.det && staged && (R == 8 || R == 16);
+    // pitched-row staging maps of the RING 38 kernel (a box of D + 8 columns needs a next head)
+    a.tma_stage = tce && p.H >= 2 && p.Hk >= 2 && 2 * G + ((R + G - 1 + 7) & ~7) + (R + G - 1) <= kQStageRows;
+    if (a.tma_stage) {
+      const int64_t kshift = int64_t(p.k2lo) * p.Hk * p.D;
+      if (!make_tmap_rows_pitched(&tmQs, qf, p.B, p.N, p.H * p.D, p.D, G) ||
+          !make_tmap_rows_pitched(&tmdOs, dof, p.B, p.N, p.H * p.D, p.D, G) ||
+          !make_tmap_rows_pitched(&tmK2s, (const __half*)k2f + kshift, p.B, p.NK(), p.Hk * p.D, p.D, R + G - 1) ||
+          !make_tmap_rows_pitched(&tmV2s, (const __half*)v2f + kshift, p.B, p.NK(), p.Hk * p.D, p.D, R + G - 1))
+        return cudaErrorInvalidValue;
+    }
 #define SA_Q_PICK(DD, DET)                                                                             \
   (gr ? SA_Q_LAUNCH(DD, DET, DET ? 129 : 130, false)                                                  \
       : (!DET && tce) ? SA_Q_LAUNCH(DD, false, 38, true)                                              \

@@ -330,5 +330,6 @@ __device__ __forceinline__ float2 bf16x2_to_f2(uint32_t u) {
 // Host: encode a 4-D [B, rows, H, D] fp16 tensor map with a (64 x 1 x box_rows x 1) box, 128B
 // swizzle (tc_host.cu).  Returns false if the driver entry point is unavailable or encoding fails.
 bool make_tmap_bnhd_f16(CUtensorMap* m, const void* base, int B, int rows, int H, int D, int box_rows);
+bool make_tmap_rows_pitched(CUtensorMap* m, const void* base, int B, int rows, int HD, int D, int box_rows);
 
 }  // namespace sa

@@ -60,6 +60,7 @@ struct FwdArgs {
   int out_f32;
   int R, G, ngroups, npairs, items;
   int det_neg;    // det with a negated scale (folded window swapped): form q x k2 = -(k2 x q)
+  int tma_stage;  // RS staged kernels: rows by pitched TMA boxes (needs H, Hk >= 2), else 1-D bulk copies
   float sm_mult;  // softmax multiplier of the raw (unscaled) logits: |s| log2(e)
 };
 
@@ -97,7 +98,8 @@ struct Smem {
   alignas(1024) uint8_t sel[RS ? kSelBytes : 16];
   float ebuf[RS ? 1 : 2][RS ? 1 : 128][17];  // generic epilogues only
   // staged bf16 rows of the next/current pair: q (2G), k2 (R+2G-1), v2 (R+2G-1); pitch D+8
-  alignas(16) __nv_bfloat16 stg[2][kStgRows][D + 8];
+  // RS: filled by three pitched-row TMA boxes; 144 rows (a multiple of 8) keep buffer 1 128-byte aligned
+  alignas(128) __nv_bfloat16 stg[2][RS ? 144 : kStgRows][D + 8];
   float rm[2][128], rl[2][128];
   float gM[2][128], gL[2][128];
   uint64_t kvfull[kSt], kvempty[kSt];
@@ -133,7 +135,9 @@ __device__ __forceinline__ int chunk_width(const Item& it, int c) {
 // their own: inlined next to the R = 32 / 64 / 128 ones they cost the larger-window kernels ~4%)
 template <int D, bool STAGED, int RS>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FwdArgs a) {
+    tc_fwd_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const __grid_constant__ CUtensorMap tmQs, const __grid_constant__ CUtensorMap tmK2s,
+                  const __grid_constant__ CUtensorMap tmV2s, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   using Sm = Smem<D, RS>;
   static_assert(sizeof(Sm) + 1024 <= 232448, "shared memory budget");
@@ -311,6 +315,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Problem& p = a.p;
     const int g = r / a.R, kk = r % a.R;
     const int nk2 = a.R + 2 * a.G - 1;  // k2/v2 rows of a pair
+    // first v2 staging row: RS kernels start each TMA box on a 128-byte boundary (pitch D + 8 halves:
+    // row offsets that are multiples of 8)
+    const int nk2p = RS != 0 ? (nk2 + 7) & ~7 : nk2;
     constexpr int kC8 = D / 8;
     // stage the rows of pair `item` into buffer `buf` (cp.async; one commit group per call)
     auto stage = [&](int item, int buf) {
@@ -320,22 +327,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kb = p.np + i0 - a.R + 1;
       const int nrows = 2 * a.G + 2 * nk2;
       if constexpr (RS != 0) {
-        // small R: one 1-D bulk copy per row (thread `row`), completing on stgfull[buf] -- the
-        // ~1.7k 16-byte cp.async of a pair are LSU-throughput bound on the softmax warps' path
-        const void* src = nullptr;
-        const int row = tid;
-        if (row < 2 * a.G) {
-          if (i0 + row < p.N) src = a.q + p.qoff(it.b, i0 + row, it.h);
-        } else if (row < nrows) {
-          const int rr = row - 2 * a.G;
-          const int kp = kb + (rr < nk2 ? rr : rr - nk2);
-          if (kp >= p.k2lo && kp < p.NK())
-            src = rr < nk2 ? (const void*)(a.k2 + p.kvoff(it.b, kp, it.hk)) : (const void*)(a.v2 + p.kvoff(it.b, kp, it.hk));
+        // small R: three TMA boxes of pitched rows (q: 2G rows, k2 / v2: nk2 rows each; rows outside
+        // the problem zero-fill), completing on stgfull[buf] -- ~1.7k 16-byte cp.async (or ~110 1-D
+        // bulk copies) per pair are issue-bound on the softmax warps' path.  k2 / v2 coordinates are
+        // real rows (the tensor maps sit on the unshifted tensors): virtual row kp is kp - k2lo.
+        if (a.tma_stage) {
+          if (tid == 0) {
+            mbar_expect_tx(&sm.stgfull[buf], uint32_t(2 * a.G + 2 * nk2) * (D + 8) * 2);
+            tma_load_4d(&sm.stg[buf][0][0], &tmQs, &sm.stgfull[buf], it.h * D, i0, it.b, 0);
+            tma_load_4d(&sm.stg[buf][2 * a.G][0], &tmK2s, &sm.stgfull[buf], it.hk * D, kb - p.k2lo, it.b, 0);
+            tma_load_4d(&sm.stg[buf][2 * a.G + nk2p][0], &tmV2s, &sm.stgfull[buf], it.hk * D, kb - p.k2lo, it.b, 0);
+          }
+          return;
         }
-        // every row is copied (rows outside the problem from a valid dummy address, never read), so
-        // one thread posts the pair's whole byte count: one expect_tx instead of ~110 arrivals
-        if (row < nrows) bulk_load(&sm.stg[buf][row][0], src ? src : (const void*)a.q, 2 * D, &sm.stgfull[buf]);
-        if (tid == 0) mbar_expect_tx(&sm.stgfull[buf], uint32_t(nrows) * 2 * D);
+        // one head (the pitched box would be wider than a row): one 1-D bulk copy per row, every row
+        // copied (rows outside the problem from a valid dummy address, never read), one expect_tx
+        const int row = tid;
+        if (row < 2 * a.G + 2 * nk2) {
+          const int rr = row - 2 * a.G;
+          const int srow = row < 2 * a.G ? row : rr < nk2 ? row : 2 * a.G + nk2p + (rr - nk2);
+          const void* src = nullptr;
+          if (row < 2 * a.G) {
+            if (i0 + row < p.N) src = a.q + p.qoff(it.b, i0 + row, it.h);
+          } else {
+            const int kp = kb + (rr < nk2 ? rr : rr - nk2);
+            if (kp >= p.k2lo && kp < p.NK())
+              src = rr < nk2 ? (const void*)(a.k2 + p.kvoff(it.b, kp, it.hk)) : (const void*)(a.v2 + p.kvoff(it.b, kp, it.hk));
+          }
+          bulk_load(&sm.stg[buf][srow][0], src ? src : (const void*)a.q, 2 * D, &sm.stgfull[buf]);
+        }
+        if (tid == 0) mbar_expect_tx(&sm.stgfull[buf], uint32_t(2 * a.G + 2 * nk2) * 2 * D);
         return;
       }
       for (int task = tid; task < nrows * kC8; task += 256) {
@@ -437,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   : a.q + p.qoff(it.b, i0 + g, it.h);
       const __half* k2row = STAGED ? reinterpret_cast<const __half*>(&sm.stg[buf][2 * a.G + srow][0])
                                    : a.k2 + p.kvoff(it.b, kpos, it.hk);
-      const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2 + srow][0] : a.v2 + p.kvoff(it.b, kpos, it.hk);
+      const __nv_bfloat16* v2row = STAGED ? &sm.stg[buf][2 * a.G + nk2p + srow][0] : a.v2 + p.kvoff(it.b, kpos, it.hk);
 
       // ---- chunks: per-row online softmax (conditional rescaling) ----
       float m_ref = -INFINITY, l = 0.f;
@@ -1012,13 +1033,24 @@ static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, cons
   a.det_neg = p.det && p.scale < 0.f ? 1 : 0;
   a.sm_mult = fabsf(p.scale) * kLog2e;
   const int grid = std::min(a.items, num_sms());
-  const bool staged = 2 * a.G + 2 * (a.R + 2 * a.G - 1) <= kStgRows;
+  const int rs = (a.R < 32 && a.R >= 2 && (a.R & (a.R - 1)) == 0) ? a.R : 0;
+  const int nk2 = a.R + 2 * a.G - 1;
+  const bool staged = 2 * a.G + (rs ? ((nk2 + 7) & ~7) : nk2) + nk2 <= kStgRows;
+  // pitched-row staging maps of the RS kernels (on the unshifted K', V' of a window-split sub-problem)
+  CUtensorMap tmQs = tmK, tmK2s = tmK, tmV2s = tmK;
+  a.tma_stage = rs && staged && p.H >= 2 && p.Hk >= 2;  // a pitched box of D + 8 columns needs a next head
+  if (a.tma_stage) {
+    const int64_t kshift = int64_t(p.k2lo) * p.Hk * p.D;
+    if (!make_tmap_rows_pitched(&tmQs, qf, p.B, p.N, p.H * p.D, p.D, 2 * a.G) ||
+        !make_tmap_rows_pitched(&tmK2s, (const __half*)k2f + kshift, p.B, p.NK(), p.Hk * p.D, p.D, nk2) ||
+        !make_tmap_rows_pitched(&tmV2s, (const __nv_bfloat16*)v2 + kshift, p.B, p.NK(), p.Hk * p.D, p.D, nk2))
+      return cudaErrorInvalidValue;
+  }
   auto launch = [&](auto kern, size_t smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     KernelScope ks("tc_fwd", st);
-    kern<<<grid, kThreads, smem, st>>>(tmK, tmV, a);
+    kern<<<grid, kThreads, smem, st>>>(tmK, tmV, tmQs, tmK2s, tmV2s, a);
   };
-  const int rs = (a.R < 32 && a.R >= 2 && (a.R & (a.R - 1)) == 0) ? a.R : 0;
   auto pick = [&](auto dc, auto sc) {
     constexpr int Dc = decltype(dc)::value;
     constexpr bool Sc = decltype(sc)::value;

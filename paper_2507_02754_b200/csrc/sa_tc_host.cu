@@ -34,6 +34,23 @@ bool make_tmap_bnhd_f16(CUtensorMap* m, const void* base, int B, int rows, int H
   return r == CUDA_SUCCESS;
 }
 
+// Row-staging map over a [B, rows, HD] tensor of 16-bit elements (HD = heads x D): box of (D + 8)
+// elements x box_rows rows, no swizzle, so a copy lands as rows of pitch D + 8 elements -- the
+// padded pitch the kernels' row-per-thread reads are bank-conflict free with.  The 8 extra columns
+// belong to the next head (or fall outside the row: zero fill) and are never read.
+bool make_tmap_rows_pitched(CUtensorMap* m, const void* base, int B, int rows, int HD, int D, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {cuuint64_t(HD), cuuint64_t(rows), cuuint64_t(B), 1};
+  cuuint64_t strides[3] = {cuuint64_t(HD) * 2, cuuint64_t(HD) * rows * 2, cuuint64_t(HD) * rows * B * 2};
+  cuuint32_t box[4] = {cuuint32_t(D + 8), cuuint32_t(box_rows), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 namespace {
 // bf16 -> fp16, 8 elements per thread-iteration.  Exact for |x| in the fp16 normal range; the
 // MMA operands must share one 16-bit format.

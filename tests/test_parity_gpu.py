@@ -201,15 +201,20 @@ def test_host_step_matches_device_path(B):
             assert torch.equal(h_out[n], dev[n].cpu()), n
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+# The memory-bound small-window point of SURVEY.md Sec. 8(d) (bench.py --sweep membound): windows 32 x 8
+# at the c3 shape, run by the R = 8 kernels (pitched-row TMA staging, tensor-core row-group sums)
+MEMBOUND = dict(B=4, H=16, N=8192, D=128, w1=32, w2=8, dtype="bf16", det=False, bwd=True)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5", "membound"])
 def test_baseline_config_sampled(cfg):
     """Full BASELINE sizes in the bench's launch configuration; the oracle checks 16 sampled
     (b, h, query-range) slices window-exactly (sa_testutil.oracle_slice).  Each slice spans
     L = w1 + 128 queries, so besides o, lse, dq (all L rows) and dk2/dv2 (L - w2 + 1 rows), 129
     interior key rows of dk/dv -- rows whose every touching query lies inside the slice -- are
     compared; the first and last slices also cover the sequence start and end."""
-    c = CONFIGS[cfg]
-    inp = make_inputs(c["B"], c["N"], c["H"], c["D"], seed_of(cfg), dtype=c["dtype"],
+    c = CONFIGS[cfg] if cfg in CONFIGS else MEMBOUND
+    inp = make_inputs(c["B"], c["N"], c["H"], c["D"], seed_of(cfg) if cfg in CONFIGS else 6000, dtype=c["dtype"],
                       device="cpu")
     got = run_cuda(inp, c["w1"], c["w2"], c["det"], bwd=c["bwd"])
     N, L = c["N"], c["w1"] + 128
