@@ -46,7 +46,9 @@ bool make_tmap_rows_pitched(CUtensorMap* m, const void* base, int B, int rows, i
   cuuint32_t box[4] = {cuuint32_t(D + 8), cuuint32_t(box_rows), 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  // no L2 promotion: the 8 padding columns touch the next head's row, which a 256-byte
+                  // promotion would pull from DRAM whole (+43% bwd_q traffic at the memory-bound point)
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
