@@ -86,17 +86,18 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // operand of the reduction MMA) and the 0/1 query-selection matrix (K-major B operand, N <= 64 rows).
 template <int D, int RS>
 struct Smem {
-  static constexpr int kSt = RS ? 2 : kStages;
+  static constexpr bool kRed = RS != 0 && RS < 32;  // tensor-core row-group sums (R <= 16)
+  static constexpr int kSt = kRed ? 2 : kStages;
   static constexpr int kPanelBytes = kChunk * 128;  // 64 rows x 64 fp16
   static constexpr int kStageBytes = kChunk * D * 2;
   static constexpr int kXBytes = 128 * 128 * 2;  // two 64-column panels even at D = 64 (the M = 128 MMA reads both)
-  static constexpr int kNSel = RS == 0 ? 16 : (128 / RS < 16 ? 16 : 128 / RS);  // reduction MMA N
+  static constexpr int kNSel = !kRed ? 16 : (128 / RS < 16 ? 16 : 128 / RS);  // reduction MMA N
   static constexpr int kSelBytes = 2 * kNSel * 128;  // 2 K-panels x kNSel query rows x 128 B
   alignas(1024) uint8_t k[kSt][kStageBytes];
   alignas(1024) uint8_t v[kSt][kStageBytes];
-  alignas(1024) uint8_t xr[RS ? 2 : 1][RS ? kXBytes : 16];
-  alignas(1024) uint8_t sel[RS ? kSelBytes : 16];
-  float ebuf[RS ? 1 : 2][RS ? 1 : 128][17];  // generic epilogues only
+  alignas(1024) uint8_t xr[kRed ? 2 : 1][kRed ? kXBytes : 16];
+  alignas(1024) uint8_t sel[kRed ? kSelBytes : 16];
+  float ebuf[RS ? 1 : 2][RS ? 1 : 128][17];  // generic / R = 64, 128 epilogues only (RS = 0)
   // staged bf16 rows of the next/current pair: q (2G), k2 (R+2G-1), v2 (R+2G-1); pitch D+8
   // RS: filled by three pitched-row TMA boxes; 144 rows (a multiple of 8) keep buffer 1 128-byte aligned
   alignas(128) __nv_bfloat16 stg[2][RS ? 144 : kStgRows][D + 8];
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == kWarpMMA) tmem_alloc<512>(&sm.tmem_base);
-  if constexpr (RS != 0) {
+  if constexpr (Sm::kRed) {
     // Sel^T [nsel query rows q][128 tile rows r] = (r / RS == q), K-major SWIZZLE_128B (2 K-panels of
     // nsel rows x 128 B); 16-byte chunk (q, c8) holds rows r = 8 c8 .. 8 c8 + 7
     for (int t = threadIdx.x; t < kNSel * 16; t += kThreads) {
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tn = item / gridDim.x;
       const bool trm = lane == 0 && tn >= 50 && tn < 52;
       SA_TRACE_AT(trm, 0, trn, tn << 16 | 10 << 8);
-      if constexpr (RS == 0) {
+      if constexpr (!Sm::kRed) {
         if (item != int(blockIdx.x)) first_s(it, kc);
       }
       for (int c = 0; c < it.nch; ++c) {
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit_w(&sm.udone[1]);
       kc += it.nch;
       ++gc;
-      if constexpr (RS != 0) {
+      if constexpr (Sm::kRed) {
         // the next item's chunk-0 S MMAs go first (its A operands are formed before this item's
         // epilogue), then the two row-group reductions O^T = X^T Sel^T of this item's epilogue into
         // the first kNSel columns of each tile's U (read out before X was published)
@@ -445,6 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = STAGED ? int(gc & 1) : 0;
       const int nitem = item + int(gridDim.x);
       // this pair's rows were staged (and waited for) before its A operands were formed; prefetch the next
+      // buffer buf ^ 1 held the previous pair, whose epilogue the other tile's warps may still be
+      // reading (v2 rows): both tiles pass this barrier before the next pair's rows overwrite it
+      if (STAGED && item != int(blockIdx.x)) named_bar_sync(3, 256);
       if (nitem < a.items) stage(nitem, buf ^ 1);
       SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 28 << 8);
       const int i0 = (2 * it.pair + x) * a.G;
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&sm.udone[x], gc & 1);
       tc_fence_after();
       SA_TRACE_AT(trs, 1 + x, trn, tn << 16 | 26 << 8);
-      if constexpr (RS != 0) {
+      if constexpr (Sm::kRed) {
         // R = RS in {2, 4, 8, 16} (kernel instances of their own): a warp holds 32/R whole queries in
         // aligned groups of R lanes; group statistics by butterfly shuffles inside the group.  The
         // R-row sum o_i = sum_k (e^{m_k - M} / L) v2_k o U_k runs on the tensor core: each thread writes
@@ -1033,7 +1037,10 @@ static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, cons
   a.det_neg = p.det && p.scale < 0.f ? 1 : 0;
   a.sm_mult = fabsf(p.scale) * kLog2e;
   const int grid = std::min(a.items, num_sms());
-  const int rs = (a.R < 32 && a.R >= 2 && (a.R & (a.R - 1)) == 0) ? a.R : 0;
+  // kernel instances: R in {2, 4, 8, 16} (tensor-core row-group sums, TMA row staging), R = 32 (TMA row
+  // staging, SA_FWD_R32_TMA=0 keeps the generic instance's cp.async staging), other R (generic)
+  static const bool r32_off = getenv("SA_FWD_R32_TMA") && atoi(getenv("SA_FWD_R32_TMA")) == 0;
+  const int rs = (a.R < 32 && a.R >= 2 && (a.R & (a.R - 1)) == 0) ? a.R : (a.R == 32 && !r32_off) ? 32 : 0;
   const int nk2 = a.R + 2 * a.G - 1;
   const bool staged = 2 * a.G + (rs ? ((nk2 + 7) & ~7) : nk2) + nk2 <= kStgRows;
   // pitched-row staging maps of the RS kernels (on the unshifted K', V' of a window-split sub-problem)
@@ -1059,6 +1066,7 @@ static cudaError_t fwd_core(const Problem& p, bool out_f32, const char* kf, cons
       case 4: launch(tc_fwd_kernel<Dc, Sc, 4>, sizeof(Smem<Dc, 4>) + 1024); break;
       case 8: launch(tc_fwd_kernel<Dc, Sc, 8>, sizeof(Smem<Dc, 8>) + 1024); break;
       case 16: launch(tc_fwd_kernel<Dc, Sc, 16>, sizeof(Smem<Dc, 16>) + 1024); break;
+      case 32: launch(tc_fwd_kernel<Dc, Sc, 32>, sizeof(Smem<Dc, 32>) + 1024); break;
       default: launch(tc_fwd_kernel<Dc, Sc, 0>, sizeof(Smem<Dc, 0>) + 1024); break;
     }
   };
