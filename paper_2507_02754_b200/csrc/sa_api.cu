@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <mutex>
 #include <stdio.h>
 #include <string.h>
@@ -337,24 +338,49 @@ sa_status simplicial_attn_host_step(const void* h_q, const void* h_k, const void
   if (scratch_bytes < need) return SA_ERR_WORKSPACE;
   bool in_f32 = flags & SA_IN_F32, out_f32 = in_f32 || (flags & SA_OUT_F32);
   const size_t nel = size_t(p.B) * p.N * p.H * p.D;
-  // Pipeline chunks: (batch b, heads [h0, h0+hc)).  Every (b,h) slice is independent.  The
-  // first and last batch elements are split into up to 8 head groups (SA_HOSTSTEP_SPLIT; measured at
-  // c3: 8 -> 31.6 ms, 4 -> 32.2, 2 -> 32.7 per step) so that the exposed first upload and last
-  // download are small; the others go whole (full-size kernel launches).  Within a chunk the forward
-  // starts once q, k, v, k2, v2 have landed (dO uploads during it) and o, lse download during the
-  // backward.
+  // Pipeline chunks: (batch b, heads [h0, h0+hc)).  Every (b,h) slice is independent.  Only
+  // the first upload and the last download are exposed, so the first batch element is cut into head
+  // groups that double (1, 2, 4, ... heads: each group's upload, ~2x faster per head than its compute,
+  // hides behind the previous group) and the last batch element into groups that halve; the other
+  // batch elements go whole (full-size launches: a 2-head chunk leaves SMs idle in bwd_kv, whose grid
+  // is key blocks x heads).  SA_HOSTSTEP_SPLIT=0: whole batch elements only.
   struct Chunk {
     int64_t b, h0, hc;
   };
   std::vector<Chunk> chunks;
-  static const int64_t max_split = getenv("SA_HOSTSTEP_SPLIT") ? atoi(getenv("SA_HOSTSTEP_SPLIT")) : 8;
-  int64_t split = 1;
-  while (split * 2 <= max_split && H % (split * 2) == 0) split *= 2;
+  static const bool no_split = getenv("SA_HOSTSTEP_SPLIT") && atoi(getenv("SA_HOSTSTEP_SPLIT")) == 0;
+  auto doubling = [&](int64_t n) {  // 1, 2, 4, ... then the remainder folded into the last group
+    std::vector<int64_t> g;
+    int64_t left = n, sz = 1;
+    while (left > 0) {
+      if (2 * sz > left - sz) {  // the next doubling would not fit: take what is left
+        g.push_back(left);
+        break;
+      }
+      g.push_back(sz);
+      left -= sz;
+      sz *= 2;
+    }
+    return g;
+  };
   for (int64_t b = 0; b < B; ++b) {
-    if (b == 0 || b == B - 1) {
-      for (int64_t q = 0; q < split; ++q) chunks.push_back({b, q * (H / split), H / split});
+    std::vector<int64_t> g;
+    if (no_split || (b > 0 && b < B - 1)) {
+      g = {H};
+    } else if (B == 1) {  // first and last: grow, then shrink
+      const std::vector<int64_t> up = doubling((H + 1) / 2);
+      std::vector<int64_t> dn = doubling(H - (H + 1) / 2);
+      g = up;
+      for (auto it = dn.rbegin(); it != dn.rend(); ++it) g.push_back(*it);
     } else {
-      chunks.push_back({b, 0, H});
+      g = doubling(H);
+      if (b == B - 1) std::reverse(g.begin(), g.end());
+    }
+    int64_t h0 = 0;
+    for (int64_t hc : g) {
+      if (hc <= 0) continue;
+      chunks.push_back({b, h0, hc});
+      h0 += hc;
     }
   }
   const size_t ein = in_f32 ? 4 : 2, eout = out_f32 ? 4 : 2;
