@@ -948,16 +948,16 @@ bool tc_fwd_supported(const Problem& p) {
 }
 
 // Window split (sa_split.cu) of a long folded window: sub-problems of <= 32 K' rows whose (o_b, lse_b)
-// are merged exactly.  Taken for w2 > 64, and for w2 > 32 when the long window is short (w1 <= 256):
-// at w2 = 64 the single tiling runs as fast as the split once w1 >= 512, where the chunk loop
-// amortises its epilogue (Table 1 sweep).  SA_FWD_WSPLIT=1 splits any
-// w2 > 32, SA_NO_WSPLIT=1 never splits.
+// are merged exactly.  Taken for every w2 > 32: the R = 32 kernel instance (TMA row staging) runs two
+// sub-windows faster than one R = 64 tiling (Table 1 (512, 64): 13.7 vs 15.5 ms forward; DESIGN.md
+// "window split").  SA_NO_WSPLIT=1 never splits (SA_FWD_WSPLIT is accepted and has no effect).
 static int fwd_split_count(const Problem& p) {
   static const bool off = getenv("SA_NO_WSPLIT") && atoi(getenv("SA_NO_WSPLIT")) != 0;
   static const bool all = getenv("SA_FWD_WSPLIT") && atoi(getenv("SA_FWD_WSPLIT")) != 0;
   const int w2 = swapped(p) ? p.w1 : p.w2, w1 = swapped(p) ? p.w2 : p.w1;
   if (off || w2 <= 32) return 1;
-  if (w2 <= 64 && w1 > 256 && !all) return 1;
+  (void)w1;
+  (void)all;
   return (w2 + 31) / 32;
 }
 static size_t fa256(size_t x) { return (x + 255) & ~size_t(255); }
