@@ -81,8 +81,8 @@ enum {
 enum { SA_PATH_SIMT = 1, SA_PATH_TCGEN05 = 2 };
 
 /* Bytes of device workspace the forward needs (the tensor-core path keeps fp16 copies of q, k, v
- * and the folded key there; a folded window over 64 rows, or over 32 with w1 <= 256, also keeps
- * the fp32 partial outputs of its <= 32-row sub-windows: the window split of DESIGN.md); 0 for
+ * and the folded key there; a folded window over 32 rows also keeps the fp32 partial outputs of
+ * its <= 32-row sub-windows: the window split of DESIGN.md); 0 for
  * the fp32 path.  The _prefixed form sizes it for n_prefix halo rows.  Returns 0 for invalid
  * arguments as well. */
 size_t simplicial_attn_fwd_workspace_bytes(int64_t B, int64_t H, int64_t N, int64_t D, int64_t w1,
