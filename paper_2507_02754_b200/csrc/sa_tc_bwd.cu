@@ -139,7 +139,7 @@ struct QSmem {
   alignas(1024) uint8_t sel[kTC ? 2 * kSelRows * 128 : 16];   // Sel^T (K-major B, two 64-row K panels)
   uint64_t red;  // kTC: completion of the epilogue's reduction MMAs (three per tile)
   uint64_t kvfull[kStages], kvempty[kStages];
-  uint64_t sfull[2], pready[2], udone, aready, stgfull[2];
+  uint64_t sfull[2], pready[2], udone, aready, stgfull[2], stgempty[2];
   uint32_t tmem_base;
 };
 
@@ -1312,6 +1312,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
     mbar_init(&sm.red, 1);
     mbar_init(&sm.stgfull[0], 1);
     mbar_init(&sm.stgfull[1], 1);
+    mbar_init(&sm.stgempty[0], 1);
+    mbar_init(&sm.stgempty[1], 1);
     fence_mbar_init();
   }
   if (warp == kQWarpMMA) tmem_alloc<512>(&sm.tmem_base);
@@ -1352,6 +1354,20 @@ __global__ void __launch_bounds__(kQThreads, 1)
       uint32_t kc = 0;
       QItem it = it_begin < it_end ? q_item(a, it_begin) : QItem{};
       for (int item = it_begin; item < it_end; ++item, it = q_item_next(a, it)) {
+        if (Sm::kTC && a.tma_stage) {
+          // RING 38 row staging of this tile (the compute warps free buffer n & 1 at the top of tile
+          // n - 1): four pitched-row TMA boxes (q, dO: G rows; k2, v2: R + G - 1 rows, the v2 box from a
+          // row that is a multiple of 8 so it starts 128-byte aligned), completing on stgfull; k2 / v2
+          // in real rows (virtual row kp is kp - k2lo)
+          const int n = item - it_begin, sb = n & 1, nk = a.R + a.G - 1;
+          mbar_wait(&sm.stgempty[sb], (n >> 1) & 1);
+          const int kb = a.p.np + it.i0 - a.R + 1 - a.p.k2lo;
+          mbar_expect_tx(&sm.stgfull[sb], uint32_t(2 * a.G + 2 * nk) * (D + 8) * 2);
+          tma_load_4d(&sm.stg[sb][0][0], &tmQs, &sm.stgfull[sb], it.h * D, it.i0, it.b, 0);
+          tma_load_4d(&sm.stg[sb][a.G][0], &tmdOs, &sm.stgfull[sb], it.h * D, it.i0, it.b, 0);
+          tma_load_4d(&sm.stg[sb][2 * a.G][0], &tmK2s, &sm.stgfull[sb], it.hk * D, kb, it.b, 0);
+          tma_load_4d(&sm.stg[sb][2 * a.G + ((nk + 7) & ~7)][0], &tmV2s, &sm.stgfull[sb], it.hk * D, kb, it.b, 0);
+        }
         for (int c = 0; c < it.nch; ++c, ++kc) {
           const int s = kc % kStages;
           const uint32_t ph = (kc / kStages) & 1;
@@ -1552,14 +1568,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
         // four pitched-row TMA boxes (q, dO: G rows; k2, v2: nk rows, the v2 box from a row that is a
         // multiple of 8 so it starts 128-byte aligned), completing on stgfull[buf]; k2 / v2 in real
         // rows (virtual row kp is kp - k2lo); lse / delta by cp.async below
-        if (tid256 == 0) {
-          const int kb = P0 - a.R + 1 - p.k2lo;
-          mbar_expect_tx(&sm.stgfull[buf], uint32_t(2 * a.G + 2 * nk) * (D + 8) * 2);
-          tma_load_4d(&sm.stg[buf][0][0], &tmQs, &sm.stgfull[buf], it.h * D, it.i0, it.b, 0);
-          tma_load_4d(&sm.stg[buf][a.G][0], &tmdOs, &sm.stgfull[buf], it.h * D, it.i0, it.b, 0);
-          tma_load_4d(&sm.stg[buf][2 * a.G][0], &tmK2s, &sm.stgfull[buf], it.hk * D, kb, it.b, 0);
-          tma_load_4d(&sm.stg[buf][2 * a.G + ((nk + 7) & ~7)][0], &tmV2s, &sm.stgfull[buf], it.hk * D, kb, it.b, 0);
-        }
+        // issued by the TMA producer warp once buffer buf is free: signal it (the compute warps are
+        // past the previous tile's end barrier, so nobody reads this buffer any more)
+        if (tid256 == 0) mbar_arrive(&sm.stgempty[buf]);
       } else
       for (int task = tid256; task < nrows * kC8; task += kQNT) {
         const int row = task / kC8, c8 = task % kC8;
