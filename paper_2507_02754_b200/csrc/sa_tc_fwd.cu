@@ -104,7 +104,7 @@ struct Smem {
   float rm[2][128], rl[2][128];
   float gM[2][128], gL[2][128];
   uint64_t kvfull[kSt], kvempty[kSt];
-  uint64_t sfull[2], pready[2], udone[2], aready[2], odone[2], stgfull[2];
+  uint64_t sfull[2], pready[2], udone[2], aready[2], odone[2], stgfull[2], stgempty[2];
   uint32_t tmem_base;
 };
 
@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.aready[x], 4);
       mbar_init(&sm.odone[x], 1);
       mbar_init(&sm.stgfull[x], 1);
+      mbar_init(&sm.stgempty[x], 1);
     }
     fence_mbar_init();
   }
@@ -197,6 +198,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t kc = 0;
       for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
         const Item it = get_item(a, item);
+        if (RS != 0 && a.tma_stage) {
+          // row staging of this pair (the softmax warps free buffer n & 1 at the top of pair n - 1):
+          // three pitched-row TMA boxes (q: 2G rows, k2 / v2: nk2 rows, the v2 box from a row that is a
+          // multiple of 8), completing on stgfull; k2 / v2 in real rows (virtual row kp is kp - k2lo)
+          const int n = (item - int(blockIdx.x)) / int(gridDim.x), sb = n & 1;
+          const int nk2 = a.R + 2 * a.G - 1, nk2p = (nk2 + 7) & ~7;
+          const int i0 = 2 * it.pair * a.G, kb = a.p.np + i0 - a.R + 1 - a.p.k2lo;
+          mbar_wait(&sm.stgempty[sb], (n >> 1) & 1);
+          mbar_expect_tx(&sm.stgfull[sb], uint32_t(2 * a.G + 2 * nk2) * (D + 8) * 2);
+          tma_load_4d(&sm.stg[sb][0][0], &tmQs, &sm.stgfull[sb], it.h * D, i0, it.b, 0);
+          tma_load_4d(&sm.stg[sb][2 * a.G][0], &tmK2s, &sm.stgfull[sb], it.hk * D, kb, it.b, 0);
+          tma_load_4d(&sm.stg[sb][2 * a.G + nk2p][0], &tmV2s, &sm.stgfull[sb], it.hk * D, kb, it.b, 0);
+        }
         for (int c = 0; c < it.nch; ++c, ++kc) {
           const int s = kc % kStages;
           const uint32_t ph = (kc / kStages) & 1;
@@ -333,12 +347,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // bulk copies) per pair are issue-bound on the softmax warps' path.  k2 / v2 coordinates are
         // real rows (the tensor maps sit on the unshifted tensors): virtual row kp is kp - k2lo.
         if (a.tma_stage) {
-          if (tid == 0) {
-            mbar_expect_tx(&sm.stgfull[buf], uint32_t(2 * a.G + 2 * nk2) * (D + 8) * 2);
-            tma_load_4d(&sm.stg[buf][0][0], &tmQs, &sm.stgfull[buf], it.h * D, i0, it.b, 0);
-            tma_load_4d(&sm.stg[buf][2 * a.G][0], &tmK2s, &sm.stgfull[buf], it.hk * D, kb - p.k2lo, it.b, 0);
-            tma_load_4d(&sm.stg[buf][2 * a.G + nk2p][0], &tmV2s, &sm.stgfull[buf], it.hk * D, kb - p.k2lo, it.b, 0);
-          }
+          // issued by the TMA producer warp once the buffer is free: signal it (both tiles are past the
+          // barrier that retires the previous pair's reads of this buffer)
+          if (tid == 0) mbar_arrive(&sm.stgempty[buf]);
           return;
         }
         // one head (the pitched box would be wider than a row): one 1-D bulk copy per row, every row
