@@ -84,6 +84,7 @@ struct BwdQArgs {
   // kk < R - Rt lie before the window and are masked like rows before the sequence start
   int out_f32, R, lR, G, ngroups, items, per_cta, ring, Rt;
   int tma_stage;  // RING 38: rows staged by pitched TMA boxes (H, Hk >= 2), else cp.async
+  int prod_stage;  // RING 37: q/dO and new k2/v2 rows by 1-D bulk copies from the TMA producer warp
   FastDiv fd_ng, fd_H, fd_ring;  // by ngroups, H, ring (per-tile index arithmetic)
 };
 
@@ -1354,6 +1355,30 @@ __global__ void __launch_bounds__(kQThreads, 1)
       uint32_t kc = 0;
       QItem it = it_begin < it_end ? q_item(a, it_begin) : QItem{};
       for (int item = it_begin; item < it_end; ++item, it = q_item_next(a, it)) {
+        if (Sm::kRing && a.prod_stage) {
+          // RING 37 row staging of this tile, off the compute warps' path: q / dO rows into buffer n & 1
+          // and the tile's new k2 / v2 rows (its whole R + G - 1 window for the first tile of a (b,h)
+          // run) into the key-position ring, one 1-D bulk copy per row, one expect_tx for the total
+          const int n = item - it_begin, sb = n & 1;
+          mbar_wait(&sm.stgempty[sb], (n >> 1) & 1);
+          const Problem& p = a.p;
+          const int P0 = p.np + it.i0;
+          const bool fresh = item == it_begin || it.grp == 0;
+          const int rh = (it.bh - a.fd_ng.div(it_begin)) & 1;
+          const int klo = fresh ? P0 - a.R + 1 : P0, khi = P0 + a.G;  // [klo, khi)
+          uint32_t bytes = 0;
+          for (int g = 0; g < it.nq; ++g) {
+            bulk_load(&sm.stgq[sb][g][0], a.q + p.qoff(it.b, it.i0 + g, it.h), 2 * D, &sm.stgfull[sb]);
+            bulk_load(&sm.stgq[sb][a.G + g][0], a.dO + p.qoff(it.b, it.i0 + g, it.h), 2 * D, &sm.stgfull[sb]);
+            bytes += 4 * D;
+          }
+          for (int kp = max(klo, p.k2lo); kp < min(khi, p.NK()); ++kp) {
+            bulk_load(&sm.rk2[rh][kp % Sm::kKR][0], a.k2 + p.kvoff(it.b, kp, it.hk), 2 * D, &sm.stgfull[sb]);
+            bulk_load(&sm.rv2[rh][kp % Sm::kKR][0], a.v2 + p.kvoff(it.b, kp, it.hk), 2 * D, &sm.stgfull[sb]);
+            bytes += 4 * D;
+          }
+          mbar_expect_tx(&sm.stgfull[sb], bytes);
+        }
         if (Sm::kTC && a.tma_stage) {
           // RING 38 row staging of this tile (the compute warps free buffer n & 1 at the top of tile
           // n - 1): four pitched-row TMA boxes (q, dO: G rows; k2, v2: R + G - 1 rows, the v2 box from a
@@ -1533,6 +1558,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const int klo = fresh ? P0 - a.R + 1 : P0;
         const int nkn = P0 + a.G - klo;  // key rows to stage
         const int nrows = 2 * a.G + 2 * nkn;
+        // producer-staged rows: signal that buffer buf (and this tile's ring slots) may be written
+        if (a.prod_stage) {
+          if (tid256 == 0) mbar_arrive(&sm.stgempty[buf]);
+        } else
         for (int task = tid256; task < nrows * kC8; task += kQNT) {
           const int row = task / kC8, c8 = task % kC8;
           const __half* src = nullptr;
@@ -1699,7 +1728,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       stage(itc, it_begin, 0);
       if (STAGED) {
         cp_async_wait<0>();
-        if (Sm::kTC && a.tma_stage) mbar_wait(&sm.stgfull[0], 0);
+        if ((Sm::kTC && a.tma_stage) || (Sm::kRing && a.prod_stage)) mbar_wait(&sm.stgfull[0], 0);
         named_bar_sync(1, kQNT);
       }
       cvt_qf(0);
@@ -1818,7 +1847,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
       // ---- A operands of the next tile (its S/dP MMAs then run during this tile's epilogue) ----
       if (item + 1 < it_end) {
         if (STAGED) cp_async_wait<0>();
-        if (Sm::kTC && a.tma_stage) mbar_wait(&sm.stgfull[buf ^ 1], ((gc + 1) >> 1) & 1);
+        if ((Sm::kTC && a.tma_stage) || (Sm::kRing && a.prod_stage))
+          mbar_wait(&sm.stgfull[buf ^ 1], ((gc + 1) >> 1) & 1);
         named_bar_sync(1, kQNT);  // every warp is past its last S/dP wait: the A regions are free
         cvt_qf(buf ^ 1);
         form_A(itn, item + 1, STAGED ? (buf ^ 1) : 0);
@@ -2893,6 +2923,12 @@ static cudaError_t bwd_core(const Problem& p, bool out_f32, const char* kf, cons
     a.band = band;
     a.gring = gring;
     a.tma_stage = 0;
+    {
+      static const bool ps_off = getenv("SA_Q_PRODSTAGE") && atoi(getenv("SA_Q_PRODSTAGE")) == 0;
+      // read by the RING 37 kernels only: measured neutral for trilinear (c3 tc_bwd_q 10.64 vs 10.72 ms)
+      // and -3.5% for the determinant variant, whose compute warps are the busier (c4 13.18 -> 12.69 ms)
+      a.prod_stage = (!ps_off && p.det) ? 1 : 0;
+    }
     a.out_f32 = out_f32 ? 1 : 0;
     a.R = R;
     a.Rt = Rt;
