@@ -2047,7 +2047,9 @@ constexpr int kKVFW = 8;                      // A-tile former warps
 constexpr int kKVF0 = 0;                      // first former warp (low ids: issue priority)
 constexpr int kKVS0 = kKVFW;                  // first softmax-gradient warp (8 warps)
 constexpr int kKVWarpMMA = 8 + kKVFW;
-constexpr int kKVThreads = 32 * (kKVWarpMMA + 1);  // warps 0-7 softmax-gradient, 8.. formers, last MMA
+constexpr int kKVWarpStg = kKVWarpMMA + 1;  // row stager: staged determinant kernels only
+constexpr int kKVThreads = 32 * (kKVWarpMMA + 1);  // warps 0-7 formers, 8-15 softmax-gradient, MMA
+constexpr int kKVThreadsStg = kKVThreads + 32;     // ... plus the stager warp
 // TMEM columns: K, V operands (D/2 packed cols each), dV, dK accumulators, 2 x (S^T, dP^T) quarters
 constexpr uint32_t kKK = 0, kKV = 64, kKdV = 128, kKdK = 256, kKSD = 384;
 constexpr int kKVRing = 40;   // staged K2/V2 rows (>= R + 2G)
@@ -2078,6 +2080,7 @@ struct KVSmem {
   // rready/rfree: direct former -> softmax handoff of rinfo[buf] (every former / softmax thread
   // arrives), so the row info does not rely on ordering carried through the MMA warp's commits
   uint64_t kvtm, aready[2], afree[2], sfull[2], pready[2], rready[2], rfree[2], done;
+  uint64_t stgfull[2], stgempty[2];  // stager warp <-> formers: tile rows landed / buffer free
   uint32_t tmem_base;
 };
 
@@ -2089,8 +2092,11 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int c8) {
 
 
 template <int D, bool DET, bool STAGED>
-__global__ void __launch_bounds__(kKVThreads, 1)
+__global__ void __launch_bounds__((DET && STAGED) ? kKVThreadsStg : kKVThreads, 1)
     tc_bwd_kv_kernel(BwdKVArgs a) {
+  // determinant formers are the busier: their row staging moves to a stager warp (c4 tc_bwd_kv
+  // 12.31 -> 11.88 ms); for the trilinear variant the formers' own cp.async staging measured faster
+  constexpr bool kStg = DET && STAGED;
   extern __shared__ uint8_t smem_raw[];
   static_assert(sizeof(KVSmem<D>) + 1024 <= 232448, "shared memory budget");
   KVSmem<D>& sm = *reinterpret_cast<KVSmem<D>*>(smem_raw + align1024_pad(smem_raw));
@@ -2117,6 +2123,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       mbar_init(&sm.rfree[s], 32 * 8);
     }
     mbar_init(&sm.done, 1);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&sm.stgfull[x], 1);
+      mbar_init(&sm.stgempty[x], 1);
+    }
     fence_mbar_init();
   }
   if (warp == kKVWarpMMA) tmem_alloc<512>(&sm.tmem_base);
@@ -2139,7 +2149,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       const int nk = khi - klo + 1;
       const int slo = ring_mod(klo);
 #pragma unroll
-      for (int which = 0; which < 2; ++which) {
+      for (int which = 0; which < 2 && !kStg; ++which) {
         for (int task = ft; task < nk * kC8; task += kNF) {
           const int off = task / kC8, c8 = task % kC8;  // kC8 is a compile-time power of two
           const int kp = klo + off;
@@ -2153,7 +2163,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       const int nq = min(a.G, qb - q0);
 #pragma unroll
-      for (int which = 0; which < 2; ++which) {
+      for (int which = 0; which < 2 && !kStg; ++which) {
         for (int task = ft; task < nq * kC8; task += kNF) {
           const int g = task / kC8, c8 = task % kC8;
           const __half* src = (which ? a.dO : a.q) + p.qoff(b, q0 + g, h) + 8 * c8;
@@ -2171,7 +2181,10 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       cp_async_commit();
     };
-    if (STAGED && ntile > 0) stage(0);
+    if (STAGED && ntile > 0) {
+      stage(0);
+      if (kStg && ft == 0) mbar_arrive(&sm.stgempty[0]);
+    }
     int trn = 0;
     for (int t = 0; t < ntile; ++t) {
       const int buf = t & 1;
@@ -2186,6 +2199,11 @@ __global__ void __launch_bounds__(kKVThreads, 1)
           cp_async_wait<0>();
         }
         named_bar_sync(2, kNF);
+        if constexpr (kStg) {
+          // every former is past tile t-1: its q/dO buffer and the ring slots tile t+1 overwrites are free
+          if (t + 1 < ntile && ft == 0) mbar_arrive(&sm.stgempty[(t + 1) & 1]);
+          mbar_wait(&sm.stgfull[buf], (t >> 1) & 1);  // tile t's rows landed
+        }
       }
       mbar_wait(&sm.afree[buf], ((t >> 1) & 1) ^ 1);
       mbar_wait(&sm.rfree[buf], ((t >> 1) & 1) ^ 1);  // softmax warps are done with rinfo[buf] of tile t-2
@@ -2495,6 +2513,33 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       SA_TRACE_AT(trf, 3, trn, t << 16 | 32 << 8);
       if (STAGED) named_bar_sync(2, kNF);  // staging buffers of tile t are free for tile t+2
     }
+  } else if (warp == kKVWarpStg) {
+    // ------------------------------ row stager (staged kernels) ------------------------------
+    // tile t's new k2/v2 ring rows (its whole window for t = 0) and q/dO rows by 1-D bulk copies, once
+    // the formers have freed them (stgempty), completing on stgfull; lse/delta stay with the formers
+    if (kStg && lane == 0) {
+      for (int t = 0; t < ntile; ++t) {
+        mbar_wait(&sm.stgempty[t & 1], (t >> 1) & 1);
+        const int q0 = qa + t * a.G, P0 = p.np + q0;
+        const int klo = t == 0 ? P0 - a.R + 1 : P0, khi = P0 + a.G - 1;
+        const int slo = a.fd_ring.mod(klo + a.ring);
+        uint32_t bytes = 0;
+        for (int kp = max(klo, p.k2lo); kp <= min(khi, p.NK() - 1); ++kp) {
+          int slot = slo + (kp - klo);
+          if (slot >= a.ring) slot -= a.ring;
+          bulk_load(&sm.rk2[slot][0], a.k2 + p.kvoff(b, kp, hkv), 2 * D, &sm.stgfull[t & 1]);
+          bulk_load(&sm.rv2[slot][0], a.v2 + p.kvoff(b, kp, hkv), 2 * D, &sm.stgfull[t & 1]);
+          bytes += 4 * D;
+        }
+        const int nq = min(a.G, qb - q0);
+        for (int g = 0; g < nq; ++g) {
+          bulk_load(&sm.sq[t & 1][g][0], a.q + p.qoff(b, q0 + g, h), 2 * D, &sm.stgfull[t & 1]);
+          bulk_load(&sm.sdo[t & 1][g][0], a.dO + p.qoff(b, q0 + g, h), 2 * D, &sm.stgfull[t & 1]);
+          bytes += 4 * D;
+        }
+        mbar_expect_tx(&sm.stgfull[t & 1], bytes);
+      }
+    }
   } else if (warp == kKVWarpMMA) {
     // ------------------------------ MMA issuer ------------------------------
     if (ntile > 0) {  // whole warp; elected lane issues
@@ -2565,7 +2610,7 @@ __global__ void __launch_bounds__(kKVThreads, 1)
       }
       mma_commit_w(&sm.done);
     }
-  } else if (warp != kKVWarpMMA) {
+  } else if (warp >= kKVS0 && warp < kKVS0 + 8) {
     // ------------------------------ P^T, dS^T and the dK/dV epilogue ------------------------------
     const int qd = warp & 3, wg = (warp - kKVS0) >> 2;
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
@@ -3040,7 +3085,7 @@ kv:
     auto launch = [&](auto kern, size_t smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       KernelScope ks("tc_bwd_kv", st);
-      kern<<<grid, kKVThreads, smem, st>>>(a);
+      kern<<<grid, (p.det && staged) ? kKVThreadsStg : kKVThreads, smem, st>>>(a);
     };
     const size_t s128 = sizeof(KVSmem<128>) + 1024, s64 = sizeof(KVSmem<64>) + 1024;
     if (p.D == 128) {
