@@ -2192,13 +2192,11 @@ __global__ void __launch_bounds__((DET && STAGED) ? kKVThreadsStg : kKVThreads, 
       const bool trf = ft == 0 && t >= 50 && t < 53;
       SA_TRACE_AT(trf, 3, trn, t << 16 | 30 << 8);
       if (STAGED) {
-        if (t + 1 < ntile) {
-          stage(t + 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
+        // tile t's rows landed (this thread's copies), then every former is past tile t-1: only now
+        // may tile t+1's rows overwrite the q/dO buffer and ring slots tile t-1 read
+        cp_async_wait<0>();
         named_bar_sync(2, kNF);
+        if (t + 1 < ntile) stage(t + 1);
         if constexpr (kStg) {
           // every former is past tile t-1: its q/dO buffer and the ring slots tile t+1 overwrites are free
           if (t + 1 < ntile && ft == 0) mbar_arrive(&sm.stgempty[(t + 1) & 1]);
