@@ -1048,18 +1048,18 @@ __device__ __forceinline__ void q_epilogue_rot_det(QSmem<D, RING, STAGED>& sm, c
 //   dq_c  = s (W x k2)_c,   dk2_c += (s q x W)_c,   dv2_c += dO_c U_c   (columns >= 3 floor(D/3): dq,
 //   dk2 contributions 0, reading R5).  The window offset o = cs - c0 (warp-uniform) selects one of three
 // compile-time index maps.
+// w[i] = W column c0 + i; k2[i], qs[i] = column cs - 4 + i (vector-loaded window), cs = c0 + O
 template <int O>
-__device__ __forceinline__ void det_cols8(const float (&w)[16], const float (&k2)[12], const float (&qs)[12],
+__device__ __forceinline__ void det_cols8(const float (&w)[16], const float (&k2)[16], const float (&qs)[16],
                                           float s, int c0, int d3, float (&v)[8], float (&ck)[8]) {
+  constexpr int kS = 4 - O;  // window index of column c0
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    constexpr int kDummy = 0;
-    (void)kDummy;
     const int t = O + j, tb = 3 * (t / 3), r = t % 3;
     const int i1 = tb + (r + 1) % 3, i2 = tb + (r + 2) % 3;
     const bool in = c0 + tb + 3 <= d3;
-    v[j] = in ? s * (w[i1] * k2[i2] - w[i2] * k2[i1]) : 0.f;
-    ck[j] = in ? qs[i1] * w[i2] - qs[i2] * w[i1] : 0.f;
+    v[j] = in ? s * (w[i1] * k2[kS + i2] - w[i2] * k2[kS + i1]) : 0.f;
+    ck[j] = in ? qs[kS + i1] * w[i2] - qs[kS + i2] * w[i1] : 0.f;
   }
 }
 
@@ -1083,17 +1083,24 @@ __device__ __forceinline__ void q_epilogue_rot_det4(QSmem<D, RING, STAGED>& sm, 
   tmem_ld8(tU + cs, uu);
 #pragma unroll
   for (int ph = 0; ph < 4; ++ph) {
-    float k2v[12], qs[12];
+    // k2 and s q over the 16-column window [cs - 4, cs + 12) (covers the chunk-aligned [c0, c0 + 12)):
+    // four 8-byte fp16 and four 16-byte fp32 loads; columns past D are masked in det_cols8
+    float k2v[16], qs[16];
     float4 fd0 = make_float4(0.f, 0.f, 0.f, 0.f), fd1 = fd0;
     float4 xk0 = fd0, xk1 = fd0, xv0 = fd0, xv1 = fd0;
 #pragma unroll
-    for (int e = 0; e < 12; ++e) k2v[e] = qs[e] = 0.f;
+    for (int e = 0; e < 16; ++e) k2v[e] = qs[e] = 0.f;
     if (valid) {
 #pragma unroll
-      for (int e = 0; e < 12; ++e) {
-        if (c0 + e < D) {
-          k2v[e] = __half2float(rw.k2[c0 + e]);
-          qs[e] = rw.qf[c0 + e];  // s q (cvt_qf)
+      for (int u = 0; u < 4; ++u) {
+        const int cw = cs - 4 + 4 * u;
+        if (cw >= 0) {
+          const uint2 h = *reinterpret_cast<const uint2*>(rw.k2 + cw);
+          const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+          const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+          k2v[4 * u] = f0.x, k2v[4 * u + 1] = f0.y, k2v[4 * u + 2] = f1.x, k2v[4 * u + 3] = f1.y;
+          const float4 q4 = *reinterpret_cast<const float4*>(rw.qf + cw);  // s q (cvt_qf)
+          qs[4 * u] = q4.x, qs[4 * u + 1] = q4.y, qs[4 * u + 2] = q4.z, qs[4 * u + 3] = q4.w;
         }
       }
       fd0 = *reinterpret_cast<const float4*>(rw.dOf + cs);
